@@ -1,0 +1,81 @@
+// Closed-shell B3LYP semi-local part, pointwise, always in f64.
+// Reference: deskdft/xc.py:200-306 (constants :200-205, weights :27-30):
+//   f = 0.08 LSDA_x + 0.72 B88_x (incl. Slater) + 0.19 VWN_c(RPA) + 0.81 LYP_c,
+// returns exc (per particle), vrho = d f / d n, vsigma = d f / d sigma; zero for
+// n < 1e-12 after clamping n, sigma >= 0.  __host__ __device__ so the CPU test
+// harness evaluates the identical arithmetic.
+#pragma once
+#include <math.h>
+
+#ifndef HD
+#define HD __host__ __device__ __forceinline__
+#endif
+
+namespace dftb {
+
+struct XCOut { double exc, vrho, vsigma; };
+
+HD XCOut b3lyp_point(double n, double sigma) {
+    const double kPi_ = 3.14159265358979323846;
+    const double CX = 0.7385587663820223;        // 3/4 (3/pi)^(1/3)
+    const double CXS = 0.9305257363491002;       // 3/2 (3/(4 pi))^(1/3)
+    const double BETA = 0.0042;
+    const double VA = 0.0310907, VB = 13.0720, VC = 42.7198, VX0 = -0.409286;
+    const double LA = 0.04918, LB = 0.132, LC = 0.2533, LD = 0.349;
+    const double CF = 2.871234000188191;        // 0.3 (3 pi^2)^(2/3)
+    XCOut o{0.0, 0.0, 0.0};
+    n = fmax(n, 0.0);
+    sigma = fmax(sigma, 0.0);
+    if (!(n >= 1e-12)) return o;
+    const double c13 = cbrt(n);
+    // Slater exchange (per particle e = -CX n^(1/3))
+    const double el = -CX * c13;
+    const double f0 = el * n, v0 = (4.0 / 3.0) * el;
+    // Becke 88 on the spin density ns = n/2, sigma_s = sigma/4
+    const double ns = 0.5 * n;
+    const double t = cbrt(ns), t4 = t * t * t * t;
+    const double x = sqrt(0.25 * sigma) / t4;
+    const double ash = asinh(x);
+    const double den = 1.0 + 6.0 * BETA * x * ash;
+    const double dden = 6.0 * BETA * (ash + x / sqrt(1.0 + x * x));
+    const double g = CXS + BETA * x * x / den;
+    const double dg = BETA * (2.0 * x * den - x * x * dden) / (den * den);
+    const double f1 = -2.0 * t4 * g;
+    const double v1 = -(4.0 / 3.0) * t * g + t4 * dg * (4.0 / 3.0) * x / ns;
+    const double w1 = 0.5 * (-BETA * (2.0 * den - x * dden) / (2.0 * den * den * t4));
+    // VWN (RPA fit, paramagnetic)
+    const double rs = cbrt(3.0 / (4.0 * kPi_ * n));
+    const double y = sqrt(rs);
+    const double Xy = rs + VB * y + VC;
+    const double X0 = VX0 * VX0 + VB * VX0 + VC;
+    const double Q = sqrt(4.0 * VC - VB * VB);
+    const double at = atan(Q / (2.0 * y + VB));
+    const double ec = VA * (log(y * y / Xy) + (2.0 * VB / Q) * at -
+                            (VB * VX0 / X0) * (log((y - VX0) * (y - VX0) / Xy) + (2.0 * (VB + 2.0 * VX0) / Q) * at));
+    const double dec = VA * (2.0 / y - 2.0 * (y + VB) / Xy -
+                             (VB * VX0 / X0) * (2.0 / (y - VX0) - 2.0 * (y + VB + VX0) / Xy));
+    const double f2 = ec * n, v2 = ec - (rs / 3.0) * dec / (2.0 * y);
+    // LYP, closed shell
+    const double tt = 1.0 / c13;                   // n^(-1/3)
+    const double Xd = 1.0 + LD * tt;
+    double tt2 = tt * tt, tt4 = tt2 * tt2, tt8 = tt4 * tt4;
+    const double om = tt8 * tt2 * tt * exp(-LC * tt) / Xd;   // t^11 e^{-c t} / X
+    const double dl = tt * (LC + LD / Xd);
+    const double n143 = n * n * n * n * cbrt(n * n);           // n^(14/3)
+    const double s37 = 3.0 + 7.0 * dl;
+    const double f3 = -LA * n / Xd - LA * LB * om * CF * n143 + LA * LB * om * n * n * sigma * s37 / 72.0;
+    const double w3 = LA * LB * om * n * n * s37 / 72.0;
+    const double tp = -tt / (3.0 * n);
+    const double omp = om * tp * (11.0 / tt - LC - LD / Xd);
+    const double dlp = tp * (LC + LD / Xd - LD * LD * tt / (Xd * Xd));
+    const double v3 = -LA / Xd + LA * n * LD * tp / (Xd * Xd) -
+                      LA * LB * CF * (omp * n143 + om * (14.0 / 3.0) * n143 / n) +
+                      (LA * LB * sigma / 72.0) * (omp * n * n * s37 + 2.0 * n * om * s37 + 7.0 * om * n * n * dlp);
+    const double ftot = 0.08 * f0 + 0.72 * f1 + 0.19 * f2 + 0.81 * f3;
+    o.exc = ftot / n;
+    o.vrho = 0.08 * v0 + 0.72 * v1 + 0.19 * v2 + 0.81 * v3;
+    o.vsigma = 0.72 * w1 + 0.81 * w3;
+    return o;
+}
+
+}  // namespace dftb

@@ -1,0 +1,141 @@
+// Shared device-side definitions for the qm1b_b200 kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <type_traits>
+
+#include "../../include/qm1b_b200.h"
+
+#define HD __host__ __device__ __forceinline__
+
+namespace dftb {
+
+constexpr int NMAX = DFTB_NMAX;
+constexpr int NPRIM = DFTB_NPRIM;
+constexpr int NPP = NPRIM * NPRIM;   // primitive pairs per shell pair
+constexpr int BOYS_NCOL = 16;        // F_m columns, m = 0..15
+constexpr int BOYS_NT = 431;         // T = 0.0 .. 43.0 step 0.1
+constexpr int PP_FIELDS = 10;        // p, Px, Py, Pz, 1/(2p), c_ss, c_sp, c_ps, c_pp, bound
+constexpr int DIIS_MAX = 8;
+constexpr int NCLS = 6;              // quartet classes (LL|LL) (LL|LS) (LL|SS) (LS|LS) (LS|SS) (SS|SS)
+
+HD int64_t tri(int64_t i) { return i * (i + 1) / 2; }
+HD int64_t pidx(int i, int j) { return i >= j ? tri(i) + j : tri(j) + i; }
+
+// Device-resident view of one batch.  Every pointer is a device pointer owned by
+// the plan (plan.cu).  Index conventions: "global" = over the whole batch,
+// "local" = within one molecule.
+struct DevBatch {
+    int n_mol, n_atom, n_shell, n_pair, n_pts;
+    int prec;                 // 0 f64, 1 f32 (ERI store + XC arithmetic)
+    // molecules
+    const int *m_nao, *m_nocc, *m_natom, *m_atom0, *m_nshell, *m_shell0, *m_pair0;
+    const int *m_npl;         // [n_mol*3] pair counts LL, LS, SS
+    const int64_t *m_mat0;    // prefix of nao^2
+    const int64_t *m_npp0;    // prefix of nao(nao+1)/2
+    const int64_t *m_eri0;    // prefix of npp(npp+1)/2
+    const int64_t *m_grid0;   // prefix of grid points
+    const int *m_jkcta0;      // prefix of J/K CTAs
+    const int *m_xccta0;      // prefix of XC CTAs
+    const int64_t *m_G0;      // prefix of tri(nao)*nao  (K partial rows)
+    const int64_t *m_Jp0;     // prefix of (ncta_jk+1)*npp (J partials)
+    const int64_t *m_V0;      // prefix of ncta_xc*nao^2 (Vxc partials)
+    const int64_t *cls0;      // [NCLS*(n_mol+1)] quartet-count prefixes per class
+    // atoms (global)
+    const int *a_z;
+    const double *a_xyz;
+    const int64_t *a_grid0;
+    const int *a_tmpl0, *a_tmpln;
+    const double *tmpl;       // [n_tmpl*4]
+    // shells (global)
+    const int *s_kind, *s_ao, *s_atom;
+    const double *s_exp, *s_cs, *s_cp;
+    // shell pairs (global); canonical orientation: L before S, else higher index first
+    const int *p_sa, *p_sb;
+    double *p_geo;            // [6][n_pair] A, B
+    double *pp;               // [PP_FIELDS][NPP][n_pair]
+    double *p_q;              // [n_pair] Schwarz bound sqrt(max (ab|ab))
+    double *qao;              // [sum npp] sqrt((ij|ij))
+    // J/K CTA table
+    const int *jk_mol, *jk_i0, *jk_i1;
+    int n_jk_cta;
+    // XC CTA table
+    const int *xc_mol;
+    const int64_t *xc_p0, *xc_p1;
+    int n_xc_cta;
+    // grid
+    double *g_xyz;            // [n_pts*3]
+    double *g_w;              // [n_pts]
+    // matrices (each sum nao^2 doubles)
+    double *S, *T, *V, *H, *X, *C, *Cp, *rho, *rho_prev, *F, *J, *K, *Vxc, *scratch;
+    double *Fring, *Ering;    // [DIIS_MAX][sum nao^2]
+    // ERI store (f64 or f32)
+    void *eri;
+    // partials
+    double *Gpart, *Jpart, *Vpart, *Epart;
+    // per-molecule scalars
+    double *enn, *hist, *comp, *Bmat, *eps;
+    int *nmo, *ring_n, *ring_head, *done, *conv, *iters, *status;
+    const double *boys;       // [BOYS_NT*BOYS_NCOL]
+    int max_it;
+};
+
+// Warp / block reductions (deterministic: fixed shuffle tree).
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Block-wide sum; `red` is >= 32 doubles of shared memory. All threads get the result.
+__device__ __forceinline__ double block_sum(double v, double *red) {
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (w == 0) {
+        t = lane < nw ? red[lane] : 0.0;
+        t = warp_sum(t);
+        if (lane == 0) red[0] = t;
+    }
+    __syncthreads();
+    t = red[0];
+    __syncthreads();
+    return t;
+}
+__device__ __forceinline__ double block_max(double v, double *red) {
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    v = warp_max(v);
+    __syncthreads();
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (w == 0) {
+        t = lane < nw ? red[lane] : 0.0;
+        t = warp_max(t);
+        if (lane == 0) red[0] = t;
+    }
+    __syncthreads();
+    t = red[0];
+    __syncthreads();
+    return t;
+}
+
+// binary search: largest m with prefix[m] <= g  (prefix has n+1 entries, prefix[0] = 0)
+__device__ __forceinline__ int find_mol(const int64_t *prefix, int n, int64_t g) {
+    int lo = 0, hi = n;  // invariant prefix[lo] <= g < prefix[hi]
+    while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (__ldg(prefix + mid) <= g) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+}  // namespace dftb

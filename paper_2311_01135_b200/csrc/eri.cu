@@ -1,0 +1,247 @@
+// Shell-pair tables, Schwarz bounds and the class-specialised ERI kernels.
+//
+// Reference path: deskdft.integrals.eri_packed (integrals.py:135-196) ->
+// _schwarz_kernel / _fill_kernel / _quartet_block (_kernels.py:350-619).
+//
+// Layout decisions (B200-first):
+//  * fused S / L(sp) shells; quartets grouped in 6 classes so every warp runs one
+//    fully-unrolled code path (template on shell kinds and on the ket component
+//    slice, which is warp-uniform because it is blockIdx.y);
+//  * primitive-pair records are SoA with the pair index fastest, so the 32 lanes of
+//    a warp (consecutive ket pairs) read one coalesced 256-byte line per field;
+//  * results go to a dense, 8-fold packed AO-pair triangle per molecule,
+//    element (P, Q) with P = ij >= Q = kl at offset P(P+1)/2 + Q: exactly the
+//    reference's canonical composite order, so the J/K digestion streams rows
+//    with no index arrays and eri_packed's canonical list is a stream compaction.
+#include "common.cuh"
+#include "md.cuh"
+
+namespace dftb {
+
+// --------------------------------------------------------------------------- pair records
+__global__ void k_pairs(DevBatch b) {
+    const int64_t pr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pr >= b.n_pair) return;
+    const int sa = b.p_sa[pr], sb = b.p_sb[pr];
+    const double *A = b.a_xyz + 3 * b.s_atom[sa];
+    const double *B = b.a_xyz + 3 * b.s_atom[sb];
+    double rab2 = 0.0;
+    for (int d = 0; d < 3; ++d) {
+        b.p_geo[(int64_t)d * b.n_pair + pr] = A[d];
+        b.p_geo[(int64_t)(3 + d) * b.n_pair + pr] = B[d];
+        rab2 += (A[d] - B[d]) * (A[d] - B[d]);
+    }
+    const int64_t np = b.n_pair;
+    for (int i = 0; i < 3; ++i) {
+        const double a = b.s_exp[3 * sa + i], csa = b.s_cs[3 * sa + i], cpa = b.s_cp[3 * sa + i];
+        for (int j = 0; j < 3; ++j) {
+            const double e = b.s_exp[3 * sb + j], csb = b.s_cs[3 * sb + j], cpb = b.s_cp[3 * sb + j];
+            const double p = a + e;
+            const double K = exp(-(a * e / p) * rab2);
+            const int k = 3 * i + j;
+            auto put = [&](int f, double v) { b.pp[((int64_t)f * 9 + k) * np + pr] = v; };
+            put(PF_P, p);
+            put(PF_X, (a * A[0] + e * B[0]) / p);
+            put(PF_Y, (a * A[1] + e * B[1]) / p);
+            put(PF_Z, (a * A[2] + e * B[2]) / p);
+            put(PF_H, 0.5 / p);
+            put(PF_CSS, csa * csb * K);
+            put(PF_CSP, csa * cpb * K);
+            put(PF_CPS, cpa * csb * K);
+            put(PF_CPP, cpa * cpb * K);
+            put(PF_BOUND, fmax(fabs(csa), fabs(cpa)) * fmax(fabs(csb), fabs(cpb)) * K);
+        }
+    }
+}
+
+// --------------------------------------------------------------------------- class geometry
+// Pair lists per molecule: [LL | LS | SS] starting at m_pair0[m].
+// class -> (bra list, ket list):  0 LL|LL  1 LL|LS  2 LL|SS  3 LS|LS  4 LS|SS  5 SS|SS
+__device__ __forceinline__ void class_lists(const DevBatch &b, int m, int cls, int &b0, int &nb,
+                                            int &k0, int &nk) {
+    const int p0 = b.m_pair0[m];
+    const int nll = b.m_npl[3 * m], nls = b.m_npl[3 * m + 1], nss = b.m_npl[3 * m + 2];
+    const int s[3] = {p0, p0 + nll, p0 + nll + nls};
+    const int n[3] = {nll, nls, nss};
+    const int bl[NCLS] = {0, 0, 0, 1, 1, 2}, kl[NCLS] = {0, 1, 2, 1, 2, 2};
+    b0 = s[bl[cls]]; nb = n[bl[cls]];
+    k0 = s[kl[cls]]; nk = n[kl[cls]];
+}
+
+__device__ __forceinline__ void decode_quartet(int cls, int64_t q, int nk, int &P, int &Q) {
+    if (cls == 0 || cls == 3 || cls == 5) {  // triangle P >= Q
+        int64_t r = (int64_t)((sqrt(8.0 * (double)q + 1.0) - 1.0) * 0.5);
+        while (tri(r + 1) <= q) ++r;
+        while (tri(r) > q) --r;
+        P = (int)r;
+        Q = (int)(q - tri(r));
+    } else {
+        P = (int)(q / nk);
+        Q = (int)(q % nk);
+    }
+}
+
+template <int N, typename F>
+__device__ __forceinline__ void static_switch(int c, F &&f) {
+    // dispatch a runtime value in [0, N) to f(integral_constant) — c is warp-uniform here
+    if constexpr (N >= 1) { if (c == 0) { f(std::integral_constant<int, 0>{}); return; } }
+    if constexpr (N >= 2) { if (c == 1) { f(std::integral_constant<int, 1>{}); return; } }
+    if constexpr (N >= 3) { if (c == 2) { f(std::integral_constant<int, 2>{}); return; } }
+    if constexpr (N >= 4) { if (c == 3) { f(std::integral_constant<int, 3>{}); return; } }
+    if constexpr (N >= 5) { if (c == 4) { f(std::integral_constant<int, 4>{}); return; } }
+    if constexpr (N >= 6) { if (c == 5) { f(std::integral_constant<int, 5>{}); return; } }
+    if constexpr (N >= 7) { if (c == 6) { f(std::integral_constant<int, 6>{}); return; } }
+    if constexpr (N >= 8) { if (c == 7) { f(std::integral_constant<int, 7>{}); return; } }
+    if constexpr (N >= 9) { if (c == 8) { f(std::integral_constant<int, 8>{}); return; } }
+    if constexpr (N >= 10) { if (c == 9) { f(std::integral_constant<int, 9>{}); return; } }
+    if constexpr (N >= 11) { if (c == 10) { f(std::integral_constant<int, 10>{}); return; } }
+    if constexpr (N >= 12) { if (c == 11) { f(std::integral_constant<int, 11>{}); return; } }
+    if constexpr (N >= 13) { if (c == 12) { f(std::integral_constant<int, 12>{}); return; } }
+    if constexpr (N >= 14) { if (c == 13) { f(std::integral_constant<int, 13>{}); return; } }
+    if constexpr (N >= 15) { if (c == 14) { f(std::integral_constant<int, 14>{}); return; } }
+    if constexpr (N >= 16) { if (c == 15) { f(std::integral_constant<int, 15>{}); return; } }
+}
+
+__device__ __forceinline__ void load_geo(const DevBatch &b, int64_t pr, double *A, double *B) {
+    for (int d = 0; d < 3; ++d) {
+        A[d] = b.p_geo[(int64_t)d * b.n_pair + pr];
+        B[d] = b.p_geo[(int64_t)(3 + d) * b.n_pair + pr];
+    }
+}
+
+template <typename ST>
+__device__ __forceinline__ void store_eri(ST *eri, int64_t base, int i, int j, int k, int l, double v) {
+    int64_t P = pidx(i, j), Q = pidx(k, l);
+    if (P < Q) { int64_t t = P; P = Q; Q = t; }
+    eri[base + tri(P) + Q] = (ST)v;
+}
+
+// --------------------------------------------------------------------------- ERI kernels
+// One thread = one screened shell quartet x one ket-component slice (blockIdx.y).
+template <int KA, int KB, int KC, int KD, int SPLIT, typename ST>
+__global__ void __launch_bounds__(128) k_eri(DevBatch b, int cls, double eps, double prim_cut, ST *eri) {
+    constexpr int NA = KA ? 4 : 1, NB = KB ? 4 : 1, NC = KC ? 4 : 1, ND = KD ? 4 : 1;
+    constexpr int NKET = NC * ND, NKS = SPLIT ? 1 : NKET, NSL = NKET / NKS;
+    const int64_t *pre = b.cls0 + (int64_t)cls * (b.n_mol + 1);
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= pre[b.n_mol]) return;
+    const int m = find_mol(pre, b.n_mol, g);
+    int b0, nb, k0, nk;
+    class_lists(b, m, cls, b0, nb, k0, nk);
+    int P, Q;
+    decode_quartet(cls, g - pre[m], nk, P, Q);
+    const int64_t Pp = b0 + P, Qp = k0 + Q;
+    if (b.p_q[Pp] * b.p_q[Qp] < eps) return;
+    double A[3], B[3], C[3], D[3];
+    load_geo(b, Pp, A, B);
+    load_geo(b, Qp, C, D);
+    const PPView V{b.pp, b.n_pair};
+    const int ia = b.s_ao[b.p_sa[Pp]], ib = b.s_ao[b.p_sb[Pp]];
+    const int ic = b.s_ao[b.p_sa[Qp]], id = b.s_ao[b.p_sb[Qp]];
+    const int64_t base = b.m_eri0[m];
+    static_switch<NSL>(blockIdx.y, [&](auto slc) {
+        constexpr int KC0 = decltype(slc)::value * NKS;
+        double out[NA * NB][NKS];
+#pragma unroll
+        for (int x = 0; x < NA * NB; ++x)
+#pragma unroll
+            for (int y = 0; y < NKS; ++y) out[x][y] = 0.0;
+        eri_quartet<KA, KB, KC, KD, KC0, NKS>(V, Pp, Qp, A, B, C, D, b.boys, prim_cut, out);
+#pragma unroll
+        for (int x = 0; x < NA * NB; ++x)
+#pragma unroll
+            for (int y = 0; y < NKS; ++y) {
+                const int kc = KC0 + y;
+                store_eri(eri, base, ia + x / NB, ib + x % NB, ic + kc / ND, id + kc % ND, out[x][y]);
+            }
+    });
+}
+
+// --------------------------------------------------------------------------- Schwarz
+// q_ao[ij] = sqrt(max(0,(ij|ij))) for every AO pair of the pair; p_q = max over the pair.
+// cls: 0 = LL pairs (16 slices, one diagonal component each), 1 = LS, 2 = SS.
+template <int KA, int KB, int SPLIT>
+__global__ void __launch_bounds__(128) k_schwarz(DevBatch b, int which) {
+    constexpr int NA = KA ? 4 : 1, NB = KB ? 4 : 1, NKET = NA * NB;
+    constexpr int NKS = SPLIT ? 1 : NKET, NSL = NKET / NKS;
+    const int64_t *pre = b.cls0 + (int64_t)(NCLS) * (b.n_mol + 1) + (int64_t)which * (b.n_mol + 1);
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= pre[b.n_mol]) return;
+    const int m = find_mol(pre, b.n_mol, g);
+    const int p0 = b.m_pair0[m] + (which >= 1 ? b.m_npl[3 * m] : 0) + (which >= 2 ? b.m_npl[3 * m + 1] : 0);
+    const int64_t Pp = p0 + (g - pre[m]);
+    double A[3], B[3];
+    load_geo(b, Pp, A, B);
+    const PPView V{b.pp, b.n_pair};
+    const int ia = b.s_ao[b.p_sa[Pp]], ib = b.s_ao[b.p_sb[Pp]];
+    double *qao = b.qao + b.m_npp0[m];
+    static_switch<NSL>(blockIdx.y, [&](auto slc) {
+        constexpr int KC0 = decltype(slc)::value * NKS;
+        double out[NKET][NKS];
+#pragma unroll
+        for (int x = 0; x < NKET; ++x)
+#pragma unroll
+            for (int y = 0; y < NKS; ++y) out[x][y] = 0.0;
+        eri_quartet<KA, KB, KA, KB, KC0, NKS>(V, Pp, Pp, A, B, A, B, b.boys, 0.0, out);
+#pragma unroll
+        for (int y = 0; y < NKS; ++y) {
+            const int c = KC0 + y;
+            const double v = out[c][y];
+            qao[pidx(ia + c / NB, ib + c % NB)] = sqrt(fmax(v, 0.0));
+        }
+    });
+}
+
+__global__ void k_pair_q(DevBatch b) {
+    const int64_t pr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pr >= b.n_pair) return;
+    // molecule of this pair: pairs are contiguous per molecule (m_pair0 prefix, int)
+    int lo = 0, hi = b.n_mol;
+    while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (b.m_pair0[mid] <= pr) lo = mid; else hi = mid;
+    }
+    const int sa = b.p_sa[pr], sb = b.p_sb[pr];
+    const int na = b.s_kind[sa] ? 4 : 1, nb = b.s_kind[sb] ? 4 : 1;
+    const int ia = b.s_ao[sa], ib = b.s_ao[sb];
+    const double *qao = b.qao + b.m_npp0[lo];
+    double q = 0.0;
+    for (int x = 0; x < na; ++x)
+        for (int y = 0; y < nb; ++y) q = fmax(q, qao[pidx(ia + x, ib + y)]);
+    b.p_q[pr] = q;
+}
+
+// --------------------------------------------------------------------------- launchers
+static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+void launch_pairs(const DevBatch &b, cudaStream_t s) {
+    if (b.n_pair) k_pairs<<<nblk(b.n_pair, 128), 128, 0, s>>>(b);
+}
+
+void launch_schwarz(const DevBatch &b, const int64_t *host_totals, cudaStream_t s) {
+    // host_totals[3]: number of LL, LS, SS pairs in the batch
+    if (host_totals[0]) k_schwarz<1, 1, 1><<<dim3(nblk(host_totals[0], 128), 16), 128, 0, s>>>(b, 0);
+    if (host_totals[1]) k_schwarz<1, 0, 0><<<dim3(nblk(host_totals[1], 128), 1), 128, 0, s>>>(b, 1);
+    if (host_totals[2]) k_schwarz<0, 0, 0><<<dim3(nblk(host_totals[2], 128), 1), 128, 0, s>>>(b, 2);
+    if (b.n_pair) k_pair_q<<<nblk(b.n_pair, 128), 128, 0, s>>>(b);
+}
+
+template <typename ST>
+static void launch_eri_t(const DevBatch &b, const int64_t *tot, double eps, double prim_cut,
+                         ST *eri, cudaStream_t s, int *nlaunch) {
+    const int T = 128;
+    if (tot[0]) { k_eri<1, 1, 1, 1, 1, ST><<<dim3(nblk(tot[0], T), 16), T, 0, s>>>(b, 0, eps, prim_cut, eri); ++*nlaunch; }
+    if (tot[1]) { k_eri<1, 1, 1, 0, 1, ST><<<dim3(nblk(tot[1], T), 4), T, 0, s>>>(b, 1, eps, prim_cut, eri); ++*nlaunch; }
+    if (tot[2]) { k_eri<1, 1, 0, 0, 0, ST><<<dim3(nblk(tot[2], T), 1), T, 0, s>>>(b, 2, eps, prim_cut, eri); ++*nlaunch; }
+    if (tot[3]) { k_eri<1, 0, 1, 0, 0, ST><<<dim3(nblk(tot[3], T), 1), T, 0, s>>>(b, 3, eps, prim_cut, eri); ++*nlaunch; }
+    if (tot[4]) { k_eri<1, 0, 0, 0, 0, ST><<<dim3(nblk(tot[4], T), 1), T, 0, s>>>(b, 4, eps, prim_cut, eri); ++*nlaunch; }
+    if (tot[5]) { k_eri<0, 0, 0, 0, 0, ST><<<dim3(nblk(tot[5], T), 1), T, 0, s>>>(b, 5, eps, prim_cut, eri); ++*nlaunch; }
+}
+
+void launch_eri(const DevBatch &b, const int64_t *tot, double eps, double prim_cut, cudaStream_t s,
+                int *nlaunch) {
+    if (b.prec == 0) launch_eri_t<double>(b, tot, eps, prim_cut, (double *)b.eri, s, nlaunch);
+    else launch_eri_t<float>(b, tot, eps, prim_cut, (float *)b.eri, s, nlaunch);
+}
+
+}  // namespace dftb

@@ -1,0 +1,634 @@
+// Device-resident SCF loop body: one CTA per molecule, everything in f64.
+//
+// Reference: deskdft.scf (scf.py:68-210): density (:68-74), fock (:77-83),
+// solve_roothaan (:86-98), diis_step (:101-132), the loop body (:168-200).
+//
+// k_orth   : eigh(S) by parallel cyclic Jacobi, keep s > 1e-7, X = U/sqrt(s)  (once)
+// k_post   : reduce J/K/Vxc partials -> F -> energies -> DIIS error + B row ->
+//            Pulay extrapolation (with the cond(B) > 1e12 damped fallback) ->
+//            X^T F X -> Jacobi (warm-started from the previous eigenvectors) ->
+//            C = X C' -> rho = 2 C_occ C_occ^T (+ pre-DIIS damping) -> convergence.
+// No host round trip: the host enqueues J/K, XC and post for every iteration.
+#include "common.cuh"
+
+namespace dftb {
+
+constexpr int SCF_THREADS = 512;
+constexpr int KP = 32;  // GEMM K-panel
+
+struct Arena {
+    double *A, *B;      // NMAX*NMAX each
+    double *sa, *sb;    // KP*NMAX each (GEMM staging)
+    double *cs, *sn;    // rotations [NMAX/2+1]
+    int *pp, *qq;       // rotation pairs
+    int *perm;          // [NMAX]
+    double *dv;         // [NMAX]
+    double *Bs;         // [10*10] DIIS system
+    double *cf;         // [10]
+    double *red;        // [32]
+    double *scal;       // [16] scalars broadcast
+};
+
+__device__ __forceinline__ Arena carve(unsigned char *base) {
+    Arena a;
+    double *p = (double *)base;
+    a.A = p; p += NMAX * NMAX;
+    a.B = p; p += NMAX * NMAX;
+    a.sa = p; p += KP * NMAX;
+    a.sb = p; p += KP * NMAX;
+    a.cs = p; p += NMAX / 2 + 2;
+    a.sn = p; p += NMAX / 2 + 2;
+    a.dv = p; p += NMAX;
+    a.Bs = p; p += 100;
+    a.cf = p; p += 10;
+    a.red = p; p += 32;
+    a.scal = p; p += 16;
+    int *q = (int *)p;
+    a.pp = q; q += NMAX / 2 + 2;
+    a.qq = q; q += NMAX / 2 + 2;
+    a.perm = q; q += NMAX;
+    return a;
+}
+
+size_t scf_smem_bytes() {
+    return sizeof(double) * (2 * NMAX * NMAX + 2 * KP * NMAX + 2 * (NMAX / 2 + 2) + NMAX + 100 + 10 + 32 + 16) +
+           sizeof(int) * (2 * (NMAX / 2 + 2) + NMAX);
+}
+
+// C (M x N, ldc) = alpha * op(A) op(B) + beta * C ; op(A) is M x K, op(B) is K x N.
+// Operands may live in global or shared memory; M, N <= NMAX.
+__device__ void cta_gemm(double *C, int ldc, const double *A, int lda, bool tA, const double *B, int ldb,
+                         bool tB, int M, int N, int K, double alpha, double beta, const Arena &ar) {
+    const int tid = threadIdx.x, ty = tid >> 5, tx = tid & 31;  // 16 x 32 threads
+    double acc[6][3];
+#pragma unroll
+    for (int a = 0; a < 6; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[a][c] = 0.0;
+    for (int k0 = 0; k0 < K; k0 += KP) {
+        const int kn = min(KP, K - k0);
+        for (int t = tid; t < KP * NMAX; t += SCF_THREADS) {
+            const int kk = t / NMAX, i = t % NMAX;
+            double va = 0.0, vb = 0.0;
+            if (kk < kn) {
+                const int k = k0 + kk;
+                if (i < M) va = tA ? A[(int64_t)k * lda + i] : A[(int64_t)i * lda + k];
+                if (i < N) vb = tB ? B[(int64_t)i * ldb + k] : B[(int64_t)k * ldb + i];
+            }
+            ar.sa[t] = va;
+            ar.sb[t] = vb;
+        }
+        __syncthreads();
+        for (int kk = 0; kk < kn; ++kk) {
+            double av[6], bv[3];
+#pragma unroll
+            for (int a = 0; a < 6; ++a) av[a] = ar.sa[kk * NMAX + ty + 16 * a];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) bv[c] = ar.sb[kk * NMAX + tx + 32 * c];
+#pragma unroll
+            for (int a = 0; a < 6; ++a)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) acc[a][c] = fma(av[a], bv[c], acc[a][c]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < 6; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int i = ty + 16 * a, j = tx + 32 * c;
+            if (i < M && j < N) {
+                double v = alpha * acc[a][c];
+                if (beta != 0.0) v += beta * C[(int64_t)i * ldc + j];
+                C[(int64_t)i * ldc + j] = v;
+            }
+        }
+    __syncthreads();
+}
+
+// Cyclic Jacobi with the round-robin (circle) ordering: n/2 disjoint rotations per
+// step, rows then columns.  A (n x n, ld n) -> diagonal; V accumulates rotations.
+__device__ void cta_jacobi(double *A, double *V, int n, const Arena &ar, int max_sweeps = 40) {
+    const int tid = threadIdx.x, nt = SCF_THREADS;
+    const int n2 = n + (n & 1), np = n2 / 2;
+    for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+        double off = 0.0, dg = 0.0;
+        for (int t = tid; t < n * n; t += nt) {
+            const int p = t / n, q = t % n;
+            if (q > p) off = fmax(off, fabs(A[t]));
+            else if (q == p) dg = fmax(dg, fabs(A[t]));
+        }
+        off = block_max(off, ar.red);
+        dg = block_max(dg, ar.red);
+        if (off <= 1e-15 * dg || off < 1e-300) break;
+        for (int r = 0; r < n2 - 1; ++r) {
+            if (tid < np) {
+                int p, q;
+                if (tid == 0) { p = r; q = n2 - 1; }
+                else { p = (r + tid) % (n2 - 1); q = (r - tid + n2 - 1) % (n2 - 1); }
+                if (p > q) { int t = p; p = q; q = t; }
+                double c = 1.0, s = 0.0;
+                if (q < n) {
+                    const double apq = A[p * n + q];
+                    if (fabs(apq) > 1e-300) {
+                        const double th = (A[q * n + q] - A[p * n + p]) / (2.0 * apq);
+                        const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+                        c = 1.0 / sqrt(t * t + 1.0);
+                        s = t * c;
+                    }
+                }
+                ar.cs[tid] = c; ar.sn[tid] = s; ar.pp[tid] = p; ar.qq[tid] = q;
+            }
+            __syncthreads();
+            for (int t = tid; t < np * n; t += nt) {
+                const int k = t / n, col = t % n;
+                const double s = ar.sn[k];
+                if (s == 0.0) continue;
+                const double c = ar.cs[k];
+                const int p = ar.pp[k], q = ar.qq[k];
+                const double ap = A[p * n + col], aq = A[q * n + col];
+                A[p * n + col] = c * ap - s * aq;
+                A[q * n + col] = s * ap + c * aq;
+            }
+            __syncthreads();
+            for (int t = tid; t < np * n; t += nt) {
+                const int k = t / n, row = t % n;
+                const double s = ar.sn[k];
+                if (s == 0.0) continue;
+                const double c = ar.cs[k];
+                const int p = ar.pp[k], q = ar.qq[k];
+                const double ap = A[row * n + p], aq = A[row * n + q];
+                A[row * n + p] = c * ap - s * aq;
+                A[row * n + q] = s * ap + c * aq;
+                const double vp = V[row * n + p], vq = V[row * n + q];
+                V[row * n + p] = c * vp - s * vq;
+                V[row * n + q] = s * vp + c * vq;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// ascending order of diag(A) -> ar.perm (rank of each original index), stable by index
+__device__ void sort_eigs(const double *A, int n, const Arena &ar) {
+    for (int i = threadIdx.x; i < n; i += SCF_THREADS) ar.dv[i] = A[i * n + i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += SCF_THREADS) {
+        const double d = ar.dv[i];
+        int r = 0;
+        for (int j = 0; j < n; ++j) {
+            const double e = ar.dv[j];
+            r += (e < d) || (e == d && j < i);
+        }
+        ar.perm[i] = r;
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------- orthogonaliser
+__global__ void __launch_bounds__(SCF_THREADS) k_orth(DevBatch b) {
+    extern __shared__ __align__(16) unsigned char ssm[];
+    const Arena ar = carve(ssm);
+    const int m = blockIdx.x, N = b.m_nao[m], tid = threadIdx.x;
+    const int64_t o = b.m_mat0[m];
+    for (int t = tid; t < N * N; t += SCF_THREADS) {
+        ar.A[t] = b.S[o + t];
+        ar.B[t] = (t / N == t % N) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    cta_jacobi(ar.A, ar.B, N, ar);
+    sort_eigs(ar.A, N, ar);
+    // kept = s > 1e-7, in ascending order: sorted positions [N - M, N)
+    if (tid == 0) {
+        int M = 0;
+        double smax = -1e300;
+        for (int i = 0; i < N; ++i) {
+            M += ar.dv[i] > 1e-7;
+            smax = fmax(smax, ar.dv[i]);
+        }
+        if (smax <= 0.0 || M == 0) b.status[m] |= DFTB_ST_OVERLAP_NOT_PD;
+        if (M < b.m_nocc[m] + 0) b.status[m] |= (M < b.m_nocc[m]) ? DFTB_ST_NO_ORBITALS : 0;
+        b.nmo[m] = M;
+        ar.scal[0] = M;
+    }
+    __syncthreads();
+    const int M = (int)ar.scal[0];
+    for (int t = tid; t < N * N; t += SCF_THREADS) {
+        const int row = t / N, i = t % N;  // eigenvector column i
+        const int r = ar.perm[i] - (N - M);
+        if (r >= 0) b.X[o + (int64_t)row * N + r] = ar.B[row * N + i] / sqrt(ar.dv[i]);
+    }
+    for (int t = tid; t < N * N; t += SCF_THREADS) {
+        const int r = t % N;
+        if (r >= M) b.X[o + t] = 0.0;
+    }
+}
+
+
+// J from owner + scattered partials, K = -(G + G^T)/4 from G rows (fixed-order sums).
+__device__ void reduce_jk(const DevBatch &b, int m, int N, double *J, double *K) {
+    const int tid = threadIdx.x;
+    const int64_t npp = tri(N);
+    const double *Jp = b.Jpart + b.m_Jp0[m];
+    const int ncj = b.m_jkcta0[m + 1] - b.m_jkcta0[m];
+    for (int64_t q = tid; q < npp; q += SCF_THREADS) {
+        double v = 0.0;
+        for (int c = 0; c <= ncj; ++c) v += Jp[(int64_t)c * npp + q];
+        int k = (int)((sqrt(8.0 * (double)q + 1.0) - 1.0) * 0.5);
+        while (tri(k + 1) <= q) ++k;
+        while (tri(k) > q) --k;
+        const int l = (int)(q - tri(k));
+        J[k * N + l] = v;
+        J[l * N + k] = v;
+    }
+    const double *Gp = b.Gpart + b.m_G0[m];
+    for (int t = tid; t < N * N; t += SCF_THREADS) {
+        const int a = t / N, c = t % N;
+        double v = 0.0;
+        for (int i = max(a, c); i < N; ++i) v += Gp[(tri(i) + a) * N + c];
+        K[t] = v;
+    }
+    __syncthreads();
+    for (int t = tid; t < N * N; t += SCF_THREADS) {
+        const int a = t / N, c = t % N;
+        if (a < c) {
+            const double g = -(K[a * N + c] + K[c * N + a]) * 0.25;
+            K[a * N + c] = g;
+            K[c * N + a] = g;
+        } else if (a == c) {
+            K[t] = -0.5 * K[t];
+        }
+    }
+}
+
+// V_xc = W + W^T with W the fixed-order sum of the per-CTA partials.
+__device__ void reduce_vxc(const DevBatch &b, int m, int N, double *Vx) {
+    const int tid = threadIdx.x;
+    const double *Vp = b.Vpart + b.m_V0[m];
+    const int ncx = b.m_xccta0[m + 1] - b.m_xccta0[m];
+    for (int t = tid; t < N * N; t += SCF_THREADS) {
+        double v = 0.0;
+        for (int c = 0; c < ncx; ++c) v += Vp[(int64_t)c * N * N + t];
+        Vx[t] = v;
+    }
+    __syncthreads();
+    for (int t = tid; t < N * N; t += SCF_THREADS) {
+        const int a = t / N, c = t % N;
+        if (a < c) {
+            const double v = Vx[a * N + c] + Vx[c * N + a];
+            Vx[a * N + c] = v;
+            Vx[c * N + a] = v;
+        } else if (a == c) {
+            Vx[t] = 2.0 * Vx[t];
+        }
+    }
+}
+
+__device__ double reduce_exc(const DevBatch &b, int m) {
+    double exc = 0.0;
+    const int ncx = b.m_xccta0[m + 1] - b.m_xccta0[m];
+    for (int c = 0; c < ncx; ++c) exc += b.Epart[b.m_xccta0[m] + c];
+    return exc;
+}
+
+// Operator-level reductions (dftb_plan_jk / dftb_plan_xc): which = 1 J/K, 2 Vxc.
+__global__ void __launch_bounds__(SCF_THREADS) k_reduce(DevBatch b, int which) {
+    const int m = blockIdx.x, N = b.m_nao[m];
+    const int64_t o = b.m_mat0[m];
+    if (which == 1) reduce_jk(b, m, N, b.J + o, b.K + o);
+    else {
+        reduce_vxc(b, m, N, b.Vxc + o);
+        if (threadIdx.x == 0) b.comp[5 * m + 4] = reduce_exc(b, m);
+    }
+}
+
+void launch_reduce(const DevBatch &b, int which, cudaStream_t s) {
+    k_reduce<<<b.n_mol, SCF_THREADS, 0, s>>>(b, which);
+}
+
+// ---------------------------------------------------------------------------- post kernel
+struct PostArgs {
+    int it;             // iteration index; -1 = core-Hamiltonian guess
+    int diis_start, diis_hist;
+    double damping, conv_std;
+};
+
+__device__ void diis_extrapolate(const DevBatch &b, int m, int N, const double *F, double *Fuse,
+                                 const PostArgs &pa, const Arena &ar) {
+    const int tid = threadIdx.x;
+    const int h = pa.diis_hist, nh = b.ring_n[m], head = b.ring_head[m];
+    const int64_t o = b.m_mat0[m], tot = b.m_mat0[b.n_mol];
+    auto slot = [&](int a) { return (head - nh + a + 2 * h) % h; };
+    if (nh <= 1) {
+        for (int t = tid; t < N * N; t += SCF_THREADS) Fuse[t] = F[t];
+        __syncthreads();
+        return;
+    }
+    const int n1 = nh + 1;
+    const double *Bm = b.Bmat + (int64_t)m * DIIS_MAX * DIIS_MAX;
+    for (int t = tid; t < n1 * n1; t += SCF_THREADS) {
+        const int r = t / n1, c = t % n1;
+        double v;
+        if (r == nh && c == nh) v = 0.0;
+        else if (r == nh || c == nh) v = 1.0;
+        else v = Bm[slot(r) * DIIS_MAX + slot(c)];
+        ar.Bs[t] = v;
+        ar.A[t] = v;
+        ar.B[t] = (r == c) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    cta_jacobi(ar.A, ar.B, n1, ar);
+    if (tid == 0) {
+        double mx = 0.0, mn = 1e308;
+        for (int i = 0; i < n1; ++i) {
+            const double e = fabs(ar.A[i * n1 + i]);
+            mx = fmax(mx, e);
+            mn = fmin(mn, e);
+        }
+        const bool fallback = !(mn > 0.0) || (mx / mn > 1e12);
+        ar.scal[1] = fallback ? 1.0 : 0.0;
+        if (!fallback) {  // Gaussian elimination with partial pivoting on the bordered system
+            double Mx[10][11];
+            for (int r = 0; r < n1; ++r) {
+                for (int c = 0; c < n1; ++c) Mx[r][c] = ar.Bs[r * n1 + c];
+                Mx[r][n1] = (r == nh) ? 1.0 : 0.0;
+            }
+            for (int c = 0; c < n1; ++c) {
+                int piv = c;
+                for (int r = c + 1; r < n1; ++r)
+                    if (fabs(Mx[r][c]) > fabs(Mx[piv][c])) piv = r;
+                if (piv != c)
+                    for (int k = 0; k <= n1; ++k) { double t = Mx[c][k]; Mx[c][k] = Mx[piv][k]; Mx[piv][k] = t; }
+                for (int r = c + 1; r < n1; ++r) {
+                    const double f = Mx[r][c] / Mx[c][c];
+                    for (int k = c; k <= n1; ++k) Mx[r][k] -= f * Mx[c][k];
+                }
+            }
+            for (int r = n1 - 1; r >= 0; --r) {
+                double s = Mx[r][n1];
+                for (int k = r + 1; k < n1; ++k) s -= Mx[r][k] * ar.cf[k];
+                ar.cf[r] = s / Mx[r][r];
+            }
+        }
+    }
+    __syncthreads();
+    if (ar.scal[1] != 0.0) {
+        const double *Fl = b.Fring + (int64_t)slot(nh - 1) * tot + o;
+        const double *Fp = b.Fring + (int64_t)slot(nh - 2) * tot + o;
+        for (int t = tid; t < N * N; t += SCF_THREADS) Fuse[t] = 0.5 * Fl[t] + 0.5 * Fp[t];
+    } else {
+        for (int t = tid; t < N * N; t += SCF_THREADS) {
+            double v = 0.0;
+            for (int a = 0; a < nh; ++a) v += ar.cf[a] * b.Fring[(int64_t)slot(a) * tot + o + t];
+            Fuse[t] = v;
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(SCF_THREADS) k_post(DevBatch b, PostArgs pa) {
+    extern __shared__ __align__(16) unsigned char ssm[];
+    const Arena ar = carve(ssm);
+    const int m = blockIdx.x, tid = threadIdx.x;
+    if (b.done[m]) return;
+    const int N = b.m_nao[m], M = b.nmo[m], nocc = b.m_nocc[m];
+    if (b.status[m] & (DFTB_ST_OVERLAP_NOT_PD | DFTB_ST_NO_ORBITALS)) {
+        if (tid == 0) b.done[m] = 1;
+        return;
+    }
+    const int64_t o = b.m_mat0[m], tot = b.m_mat0[b.n_mol];
+    double *S = b.S + o, *H = b.H + o, *X = b.X + o, *C = b.C + o, *Cp = b.Cp + o;
+    double *rho = b.rho + o, *F = b.F + o, *J = b.J + o, *K = b.K + o, *Vx = b.Vxc + o;
+    double *S1 = b.scratch + o, *S2 = b.scratch + tot + o;
+    const int it = pa.it;
+    const double *Fuse = H;
+    if (it >= 0) {
+        reduce_jk(b, m, N, J, K);
+        reduce_vxc(b, m, N, Vx);
+        __syncthreads();
+        // (4) F and (5) energies
+        double ec = 0.0, ej = 0.0, ek = 0.0;
+        for (int t = tid; t < N * N; t += SCF_THREADS) {
+            const double f = H[t] + J[t] + 0.20 * K[t] + Vx[t];
+            F[t] = f;
+            ec += rho[t] * H[t];
+            ej += rho[t] * J[t];
+            ek += rho[t] * K[t];
+        }
+        ec = block_sum(ec, ar.red);
+        ej = block_sum(ej, ar.red);
+        ek = block_sum(ek, ar.red);
+        if (tid == 0) {
+            const double exc = reduce_exc(b, m);
+            double *cp = b.comp + 5 * m;
+            cp[0] = b.enn[m];
+            cp[1] = ec;
+            cp[2] = 0.5 * ej;
+            cp[3] = 0.5 * 0.20 * ek;
+            cp[4] = exc;
+            b.hist[(int64_t)m * b.max_it + it] = cp[0] + cp[1] + cp[2] + cp[3] + cp[4];
+        }
+        // (6) DIIS error e = F rho S - S rho F = A - A^T with A = F rho S
+        cta_gemm(S1, N, F, N, false, rho, N, false, N, N, N, 1.0, 0.0, ar);
+        cta_gemm(S2, N, S1, N, false, S, N, false, N, N, N, 1.0, 0.0, ar);
+        const int h = pa.diis_hist, head = b.ring_head[m];
+        double *Fs = b.Fring + (int64_t)head * tot + o, *Es = b.Ering + (int64_t)head * tot + o;
+        for (int t = tid; t < N * N; t += SCF_THREADS) {
+            const int a = t / N, c = t % N;
+            Es[t] = S2[a * N + c] - S2[c * N + a];
+            Fs[t] = F[t];
+        }
+        __syncthreads();
+        // (7) B row for the new entry against every stored error (physical slots)
+        const int nh_new = min(b.ring_n[m] + 1, h);
+        double *Bm = b.Bmat + (int64_t)m * DIIS_MAX * DIIS_MAX;
+        for (int a = 0; a < nh_new; ++a) {
+            const int sl = (head - a + h) % h;  // walk back from the newest
+            const double *Ea = b.Ering + (int64_t)sl * tot + o;
+            double d = 0.0;
+            for (int t = tid; t < N * N; t += SCF_THREADS) d += Es[t] * Ea[t];
+            d = block_sum(d, ar.red);
+            if (tid == 0) {
+                Bm[head * DIIS_MAX + sl] = d;
+                Bm[sl * DIIS_MAX + head] = d;
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            b.ring_head[m] = (head + 1) % h;
+            b.ring_n[m] = nh_new;
+        }
+        __syncthreads();
+        // (8) extrapolation
+        if (it + 1 >= pa.diis_start) {
+            diis_extrapolate(b, m, N, F, S1, pa, ar);
+            Fuse = S1;
+        } else {
+            Fuse = F;
+        }
+    }
+    // (9) Roothaan: F' = X^T F X, Jacobi (warm start from previous C'), C = X C'
+    cta_gemm(S2, N, Fuse, N, false, X, N, false, N, M, N, 1.0, 0.0, ar);     // F X  (N x M, ld N)
+    cta_gemm(ar.A, M, X, N, true, S2, N, false, M, M, N, 1.0, 0.0, ar);      // X^T (F X)
+    if (it >= 0) {
+        cta_gemm(S1, M, ar.A, M, false, Cp, M, false, M, M, M, 1.0, 0.0, ar); // F' C'
+        cta_gemm(ar.A, M, Cp, M, true, S1, M, false, M, M, M, 1.0, 0.0, ar);  // C'^T F' C'
+        for (int t = tid; t < M * M; t += SCF_THREADS) ar.B[t] = Cp[t];
+    } else {
+        for (int t = tid; t < M * M; t += SCF_THREADS) ar.B[t] = (t / M == t % M) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    cta_jacobi(ar.A, ar.B, M, ar);
+    sort_eigs(ar.A, M, ar);
+    for (int t = tid; t < M * M; t += SCF_THREADS) {
+        const int row = t / M, i = t % M;
+        Cp[row * M + ar.perm[i]] = ar.B[t];
+    }
+    for (int i = tid; i < M; i += SCF_THREADS) b.eps[(int64_t)m * NMAX + ar.perm[i]] = ar.dv[i];
+    __syncthreads();
+    cta_gemm(C, N, X, N, false, Cp, M, false, N, M, M, 1.0, 0.0, ar);         // C = X C' (N x M)
+    // rho_new = 2 C_occ C_occ^T (+ damping when the next iteration is pre-DIIS)
+    cta_gemm(S2, N, C, N, false, C, N, true, N, N, nocc, 2.0, 0.0, ar);
+    const int nxt = it + 1;
+    const bool damp = nxt > 0 && nxt < pa.diis_start;
+    const double d = pa.damping;
+    for (int t = tid; t < N * N; t += SCF_THREADS) {
+        double v = S2[t];
+        if (damp) v = d * rho[t] + (1.0 - d) * v;
+        if (b.prec) v = (double)(float)v;
+        rho[t] = v;
+    }
+    if (tid == 0 && it >= 0) {
+        b.iters[m] = it + 1;
+        bool stop = (it + 1 >= b.max_it);
+        if (it + 1 >= 5) {
+            const double *hh = b.hist + (int64_t)m * b.max_it + it - 4;
+            double mean = 0.0;
+            for (int k = 0; k < 5; ++k) mean += hh[k];
+            mean /= 5.0;
+            double var = 0.0;
+            for (int k = 0; k < 5; ++k) var += (hh[k] - mean) * (hh[k] - mean);
+            if (sqrt(var / 5.0) < pa.conv_std) {
+                b.conv[m] = 1;
+                stop = true;
+            }
+        }
+        if (stop) b.done[m] = 1;
+    }
+}
+
+void launch_orth(const DevBatch &b, cudaStream_t s) {
+    const size_t sm = scf_smem_bytes();
+    cudaFuncSetAttribute(k_orth, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_orth<<<b.n_mol, SCF_THREADS, sm, s>>>(b);
+}
+
+void launch_post(const DevBatch &b, int it, int diis_start, int diis_hist, double damping, double conv_std,
+                 cudaStream_t s) {
+    const size_t sm = scf_smem_bytes();
+    cudaFuncSetAttribute(k_post, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    PostArgs pa{it, diis_start, diis_hist, damping, conv_std};
+    k_post<<<b.n_mol, SCF_THREADS, sm, s>>>(b, pa);
+}
+
+// ---------------------------------------------------------------------------- standalone roothaan
+// For the operator-level API: F given per molecule in b.F; writes C, eps (cold Jacobi).
+__global__ void __launch_bounds__(SCF_THREADS) k_roothaan(DevBatch b) {
+    extern __shared__ __align__(16) unsigned char ssm[];
+    const Arena ar = carve(ssm);
+    const int m = blockIdx.x, tid = threadIdx.x;
+    const int N = b.m_nao[m], M = b.nmo[m];
+    const int64_t o = b.m_mat0[m], tot = b.m_mat0[b.n_mol];
+    double *X = b.X + o, *C = b.C + o, *Cp = b.Cp + o, *S2 = b.scratch + tot + o;
+    cta_gemm(S2, N, b.F + o, N, false, X, N, false, N, M, N, 1.0, 0.0, ar);
+    cta_gemm(ar.A, M, X, N, true, S2, N, false, M, M, N, 1.0, 0.0, ar);
+    for (int t = tid; t < M * M; t += SCF_THREADS) ar.B[t] = (t / M == t % M) ? 1.0 : 0.0;
+    __syncthreads();
+    cta_jacobi(ar.A, ar.B, M, ar);
+    sort_eigs(ar.A, M, ar);
+    for (int t = tid; t < M * M; t += SCF_THREADS) Cp[(t / M) * M + ar.perm[t % M]] = ar.B[t];
+    for (int i = tid; i < M; i += SCF_THREADS) b.eps[(int64_t)m * NMAX + ar.perm[i]] = ar.dv[i];
+    __syncthreads();
+    cta_gemm(C, N, X, N, false, Cp, M, false, N, M, M, 1.0, 0.0, ar);
+}
+
+void launch_roothaan(const DevBatch &b, cudaStream_t s) {
+    const size_t sm = scf_smem_bytes();
+    cudaFuncSetAttribute(k_roothaan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_roothaan<<<b.n_mol, SCF_THREADS, sm, s>>>(b);
+}
+
+// ---------------------------------------------------------------------------- standalone DIIS
+// One system: F, E given as m x (n x n) arrays; out = diis_step(history) (scf.py:101-132).
+__global__ void __launch_bounds__(SCF_THREADS) k_diis_single(const double *F, const double *E, int mh, int n,
+                                                            double *out) {
+    extern __shared__ __align__(16) unsigned char ssm[];
+    const Arena ar = carve(ssm);
+    const int tid = threadIdx.x, nn = n * n;
+    if (mh == 1) {
+        for (int t = tid; t < nn; t += SCF_THREADS) out[t] = F[t];
+        return;
+    }
+    const int n1 = mh + 1;
+    for (int a = 0; a < mh; ++a)
+        for (int c = a; c < mh; ++c) {
+            double d = 0.0;
+            for (int t = tid; t < nn; t += SCF_THREADS) d += E[(int64_t)a * nn + t] * E[(int64_t)c * nn + t];
+            d = block_sum(d, ar.red);
+            if (tid == 0) { ar.Bs[a * n1 + c] = d; ar.Bs[c * n1 + a] = d; }
+        }
+    __syncthreads();
+    for (int t = tid; t < n1 * n1; t += SCF_THREADS) {
+        const int r = t / n1, c = t % n1;
+        if (r == mh || c == mh) ar.Bs[t] = (r == mh && c == mh) ? 0.0 : 1.0;
+    }
+    __syncthreads();
+    for (int t = tid; t < n1 * n1; t += SCF_THREADS) {
+        ar.A[t] = ar.Bs[t];
+        ar.B[t] = (t / n1 == t % n1) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    cta_jacobi(ar.A, ar.B, n1, ar);
+    if (tid == 0) {
+        double mx = 0.0, mn = 1e308;
+        for (int i = 0; i < n1; ++i) { const double e = fabs(ar.A[i * n1 + i]); mx = fmax(mx, e); mn = fmin(mn, e); }
+        const bool fb = !(mn > 0.0) || (mx / mn > 1e12);
+        ar.scal[1] = fb;
+        if (!fb) {
+            double Mx[10][11];
+            for (int r = 0; r < n1; ++r) {
+                for (int c = 0; c < n1; ++c) Mx[r][c] = ar.Bs[r * n1 + c];
+                Mx[r][n1] = (r == mh) ? 1.0 : 0.0;
+            }
+            for (int c = 0; c < n1; ++c) {
+                int piv = c;
+                for (int r = c + 1; r < n1; ++r) if (fabs(Mx[r][c]) > fabs(Mx[piv][c])) piv = r;
+                if (piv != c) for (int k = 0; k <= n1; ++k) { double t = Mx[c][k]; Mx[c][k] = Mx[piv][k]; Mx[piv][k] = t; }
+                for (int r = c + 1; r < n1; ++r) {
+                    const double f = Mx[r][c] / Mx[c][c];
+                    for (int k = c; k <= n1; ++k) Mx[r][k] -= f * Mx[c][k];
+                }
+            }
+            for (int r = n1 - 1; r >= 0; --r) {
+                double s = Mx[r][n1];
+                for (int k = r + 1; k < n1; ++k) s -= Mx[r][k] * ar.cf[k];
+                ar.cf[r] = s / Mx[r][r];
+            }
+        }
+    }
+    __syncthreads();
+    for (int t = tid; t < nn; t += SCF_THREADS) {
+        double v = 0.0;
+        if (ar.scal[1] != 0.0) v = 0.5 * F[(int64_t)(mh - 1) * nn + t] + 0.5 * F[(int64_t)(mh - 2) * nn + t];
+        else for (int a = 0; a < mh; ++a) v += ar.cf[a] * F[(int64_t)a * nn + t];
+        out[t] = v;
+    }
+}
+
+void launch_diis_single(const double *F, const double *E, int mh, int n, double *out, cudaStream_t s) {
+    const size_t sm = scf_smem_bytes();
+    cudaFuncSetAttribute(k_diis_single, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_diis_single<<<1, SCF_THREADS, sm, s>>>(F, E, mh, n, out);
+}
+
+}  // namespace dftb
