@@ -21,6 +21,13 @@ constexpr int NCLS = 6;              // quartet classes (LL|LL) (LL|LS) (LL|SS) 
 
 HD int64_t tri(int64_t i) { return i * (i + 1) / 2; }
 HD int64_t pidx(int i, int j) { return i >= j ? tri(i) + j : tri(j) + i; }
+// ERI store rows are padded to 16 bytes (g elements: 4 for f32, 2 for f64) so every row
+// can be fetched with one cp.async.bulk.  Row P (P+1 entries) starts at rowbase(P, g).
+HD int64_t rowpad(int64_t len, int g) { return (len + g - 1) / g * g; }
+HD int64_t rowbase(int64_t P, int g) {
+    const int64_t a = P / g, r = P % g;
+    return (int64_t)g * (g * a * (a + 1) / 2 + r * (a + 1));
+}
 
 // Device-resident view of one batch.  Every pointer is a device pointer owned by
 // the plan (plan.cu).  Index conventions: "global" = over the whole batch,
@@ -78,6 +85,7 @@ struct DevBatch {
     int *nmo, *ring_n, *ring_head, *done, *conv, *iters, *status;
     const double *boys;       // [BOYS_NT*BOYS_NCOL]
     int max_it;
+    long long *dbg;           // [n_mol*16] phase cycle counters (diagnostics)
 };
 
 // Warp / block reductions (deterministic: fixed shuffle tree).

@@ -5,99 +5,200 @@
 //
 // B200 formulation ("row owner"): a CTA owns the store rows P = (i, j), j <= i,
 // for one or two values of i.  Row P holds (ij|kl) for all Q = (k, l) <= P.  For a
-// stored element, the 8 images contribute J_P += v rho~_Q, J_Q += v rho~_P and,
-// recording each K contribution at (a,d) or its transpose, G[i][.] and G[j][.]
-// updates only (K = -(G + G^T)/4 at the end).  So per row the CTA expands the row
-// into a symmetric N x N smem tile T and computes two GEMVs (T rho_j, T rho_i) plus
-// one dot product; G rows for the owned i accumulate in registers, the j rows
-// and the scattered J entries are written as partials and summed in a fixed order
-// by the SCF post kernel.  The store is streamed exactly once per iteration.
+// stored element the 8 images contribute J_P += v rho~_Q, J_Q += v rho~_P and —
+// recording each K contribution at (a,d) or its transpose — only G[i][.] and G[j][.]
+// updates (K = -(G + G^T)/4 at the end).  Per row the CTA expands the row into a
+// symmetric N x N shared tile T and computes two GEMVs (T rho_j, T rho_i) and one
+// dot product.  G_i accumulates in registers across the CTA's rows, the J_Q
+// scatter accumulates in registers (thread t owns Q = t mod 256), G_j rows and J
+// partials are written once and summed in a fixed order by the SCF post kernel.
+//
+// Data movement: rows are 16-byte padded in HBM and prefetched whole with
+// cp.async.bulk (TMA bulk copy, mbarrier completion) into a double-buffered
+// staging area while the previous row is being digested; the store is streamed
+// exactly once per SCF iteration.  In the f32 build the rho / T tiles are kept in
+// f32 shared memory (rho is f32-valued there), products are formed in f64.
 #include "common.cuh"
 
 namespace dftb {
 
-template <typename ST>
-__global__ void __launch_bounds__(128) k_jk(DevBatch b) {
-    extern __shared__ double sm[];
+constexpr int JK_THREADS = 256;
+constexpr int JK_NREG = (NMAX * (NMAX + 1) / 2 + JK_THREADS - 1) / JK_THREADS;  // owned J_Q slots
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bulk_row(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+struct JKLayout {
+    size_t stage, rho, T, lut, wpart, total;
+};
+
+template <typename ST, typename RT>
+HD JKLayout jk_layout(int N, int nbuf) {
+    const int g = 16 / (int)sizeof(ST);
+    const size_t npp = (size_t)N * (N + 1) / 2;
+    JKLayout L;
+    size_t o = 64;                                    // mbarriers
+    L.stage = o; o += (size_t)nbuf * rowpad((int64_t)npp, g) * sizeof(ST);
+    o = (o + 15) & ~(size_t)15;
+    L.rho = o; o += (size_t)N * N * sizeof(RT);
+    L.T = o; o += (size_t)N * N * sizeof(RT);
+    o = (o + 15) & ~(size_t)15;
+    L.lut = o; o += npp * sizeof(uint16_t);
+    o = (o + 15) & ~(size_t)15;
+    L.wpart = o; o += 8 * sizeof(double);
+    L.total = o;
+    return L;
+}
+
+template <typename ST, typename RT>
+__global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, int nbuf) {
+    extern __shared__ __align__(128) unsigned char sm[];
     const int cta = blockIdx.x;
     const int m = b.jk_mol[cta];
     if (b.done[m]) return;
     const int N = b.m_nao[m];
+    const int g = 16 / (int)sizeof(ST);
     const int64_t npp = tri(N);
-    double *rho = sm;                 // N*N
-    double *Tm = rho + N * N;         // N*N
-    double *Jsc = Tm + N * N;         // npp
-    double *red = Jsc + npp;          // 32
-    int *lut = (int *)(red + 32);     // npp  (k << 8 | l)
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const double *rg = b.rho + b.m_mat0[m];
-    for (int t = tid; t < N * N; t += nt) rho[t] = rg[t];
-    for (int t = tid; t < npp; t += nt) Jsc[t] = 0.0;
-    for (int k = tid; k < N; k += nt)
-        for (int l = 0; l <= k; ++l) lut[tri(k) + l] = (k << 8) | l;
-    __syncthreads();
+    const JKLayout L = jk_layout<ST, RT>(N, nbuf);
+    uint64_t *bar = (uint64_t *)sm;
+    ST *stage = (ST *)(sm + L.stage);
+    const int64_t stride = rowpad(npp, g);
+    RT *rho = (RT *)(sm + L.rho);
+    RT *Tm = (RT *)(sm + L.T);
+    uint16_t *lut = (uint16_t *)(sm + L.lut);
+    double *wpart = (double *)(sm + L.wpart);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const ST *eri = (const ST *)b.eri + b.m_eri0[m];
+    const int i0 = b.jk_i0[cta], i1 = b.jk_i1[cta];
+    const int nrow0 = i0 + 1, nrows = nrow0 + (i1 >= 0 ? i1 + 1 : 0);
+    auto row_ij = [&](int r, int &i, int &j) {
+        if (r < nrow0) { i = i0; j = r; } else { i = i1; j = r - nrow0; }
+    };
+    auto issue = [&](int r) {
+        int i, j;
+        row_ij(r, i, j);
+        const int64_t P = tri(i) + j;
+        bulk_row(stage + (r % nbuf) * stride, eri + rowbase(P, g), (uint32_t)(rowpad(P + 1, g) * sizeof(ST)),
+                 bar + (r % nbuf));
+    };
+    if (tid == 0) {
+        for (int k = 0; k < nbuf; ++k) mbar_init(bar + k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int r = 0; r < nbuf && r < nrows; ++r) issue(r);
+    const double *rg = b.rho + b.m_mat0[m];
+    for (int t = tid; t < N * N; t += JK_THREADS) rho[t] = (RT)rg[t];
+    for (int k = tid; k < N; k += JK_THREADS)
+        for (int l = 0; l <= k; ++l) lut[tri(k) + l] = (uint16_t)((k << 8) | l);
+    __syncthreads();
+    double jsc[JK_NREG];
+#pragma unroll
+    for (int q = 0; q < JK_NREG; ++q) jsc[q] = 0.0;
     double *Gp = b.Gpart + b.m_G0[m];
     double *Jp = b.Jpart + b.m_Jp0[m];
-    const int local = cta - b.m_jkcta0[m];
-    const int iv[2] = {b.jk_i0[cta], b.jk_i1[cta]};
-    for (int s = 0; s < 2; ++s) {
-        const int i = iv[s];
-        if (i < 0) continue;
-        double gi = 0.0;
-        for (int j = 0; j <= i; ++j) {
-            const int64_t P = tri(i) + j;
-            const ST *row = eri + tri(P);
-            const double rt = rho[i * N + j] * (i != j ? 2.0 : 1.0);
-            double jown = 0.0;
-            for (int64_t e = tid; e <= P; e += nt) {
+    double gi = 0.0;
+    for (int r = 0; r < nrows; ++r) {
+        int i, j;
+        row_ij(r, i, j);
+        const int64_t P = tri(i) + j;
+        const ST *row = stage + (r % nbuf) * stride;
+        mbar_wait(bar + (r % nbuf), (uint32_t)((r / nbuf) & 1));
+        // ---- phase 1: expand the row into T, J_own dot product, scattered J_Q
+        const double rt = (double)rho[i * N + j] * (i != j ? 2.0 : 1.0);
+        double jown = 0.0;
+#pragma unroll
+        for (int q = 0; q < JK_NREG; ++q) {
+            const int64_t e = tid + (int64_t)q * JK_THREADS;
+            if (e <= P) {
                 const double v = (double)row[e];
                 const int kl = lut[e], k = kl >> 8, l = kl & 255;
-                const double c = e == P ? v : 2.0 * v;
+                const RT c = (RT)(e == P ? v : 2.0 * v);
                 Tm[k * N + l] = c;
                 Tm[l * N + k] = c;
-                jown += v * rho[k * N + l] * (k != l ? 2.0 : 1.0);
-                if (e < P) Jsc[e] += v * rt;
+                jown += v * (double)rho[k * N + l] * (k != l ? 2.0 : 1.0);
+                if (e < P) jsc[q] += v * rt;
             }
-            for (int l = j + 1 + tid; l <= i; l += nt) {
-                Tm[i * N + l] = 0.0;
-                Tm[l * N + i] = 0.0;
-            }
-            jown = block_sum(jown, red);  // also orders the Tm writes before the reads below
-            if (tid == 0) Jp[P] = jown;
-            if (tid <= i) {
-                double a = 0.0, c2 = 0.0;
-                const double *rj = rho + j * N, *ri = rho + i * N;
-                for (int n = 0; n <= i; ++n) {
-                    const double tv = Tm[n * N + tid];
-                    a += tv * rj[n];
-                    c2 += tv * ri[n];
-                }
-                gi += a;
-                if (j < i) Gp[P * N + tid] = c2;
-            }
-            __syncthreads();
         }
-        if (tid <= i) Gp[(tri(i) + i) * N + tid] = gi;
+        for (int l = j + 1 + tid; l <= i; l += JK_THREADS) {
+            Tm[i * N + l] = (RT)0;
+            Tm[l * N + i] = (RT)0;
+        }
+        jown = warp_sum(jown);
+        if (lane == 0) wpart[warp] = jown;
+        __syncthreads();
+        if (tid == 0) {
+            double s = 0.0;
+            for (int w = 0; w < JK_THREADS / 32; ++w) s += wpart[w];
+            Jp[P] = s;
+            if (r + nbuf < nrows) issue(r + nbuf);   // this row's staging buffer is free again
+        }
+        // ---- phase 2: G_i[t] += (T rho_j)[t] (threads 0..i), G_j[t] = (T rho_i)[t] (threads 128..)
+        if (tid <= i) {
+            double a = 0.0;
+            const RT *rj = rho + j * N;
+            for (int n = 0; n <= i; ++n) a += (double)Tm[n * N + tid] * (double)rj[n];
+            gi += a;
+        } else if (tid >= 128 && tid - 128 <= i && j < i) {
+            const int t = tid - 128;
+            double c2 = 0.0;
+            const RT *ri = rho + i * N;
+            for (int n = 0; n <= i; ++n) c2 += (double)Tm[n * N + t] * (double)ri[n];
+            Gp[P * N + t] = c2;
+        }
+        if (j == i) {
+            if (tid <= i) Gp[(tri(i) + i) * N + tid] = gi;
+            gi = 0.0;
+        }
+        __syncthreads();
     }
+    const int local = cta - b.m_jkcta0[m];
     double *Js = Jp + (int64_t)(1 + local) * npp;
-    for (int64_t t = tid; t < npp; t += nt) Js[t] = Jsc[t];
+#pragma unroll
+    for (int q = 0; q < JK_NREG; ++q) {
+        const int64_t e = tid + (int64_t)q * JK_THREADS;
+        if (e < npp) Js[e] = jsc[q];
+    }
 }
 
-size_t jk_smem_bytes(int nmax) {
-    const size_t npp = (size_t)nmax * (nmax + 1) / 2;
-    return sizeof(double) * (2 * (size_t)nmax * nmax + npp + 32) + sizeof(int) * npp;
+template <typename ST, typename RT>
+static void launch_jk_t(const DevBatch &b, int nmax, cudaStream_t s) {
+    int nbuf = 2;
+    size_t sm = jk_layout<ST, RT>(nmax, 2).total;
+    if (sm > 227 * 1024) {
+        nbuf = 1;
+        sm = jk_layout<ST, RT>(nmax, 1).total;
+    }
+    cudaFuncSetAttribute(k_jk<ST, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_jk<ST, RT><<<b.n_jk_cta, JK_THREADS, sm, s>>>(b, nbuf);
 }
 
 void launch_jk(const DevBatch &b, int nmax, cudaStream_t s) {
-    const size_t sm = jk_smem_bytes(nmax);
-    if (b.prec == 0) {
-        cudaFuncSetAttribute(k_jk<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_jk<double><<<b.n_jk_cta, 128, sm, s>>>(b);
-    } else {
-        cudaFuncSetAttribute(k_jk<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_jk<float><<<b.n_jk_cta, 128, sm, s>>>(b);
-    }
+    if (b.prec == 0) launch_jk_t<double, double>(b, nmax, s);
+    else launch_jk_t<float, float>(b, nmax, s);
 }
 
 }  // namespace dftb

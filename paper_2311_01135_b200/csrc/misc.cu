@@ -80,7 +80,7 @@ __global__ void k_compact(DevBatch b, int mol, double eps, const double *qsp, in
                           double *ov) {
     __shared__ int64_t scan[128];
     const int64_t P = blockIdx.x;
-    const ST *row = (const ST *)b.eri + b.m_eri0[mol] + tri(P);
+    const ST *row = (const ST *)b.eri + b.m_eri0[mol] + rowbase(P, 16 / (int)sizeof(ST));
     const double *qao = b.qao + b.m_npp0[mol];
     const int64_t len = P + 1, per = (len + 127) / 128;
     const int64_t lo = threadIdx.x * per, hi = min(len, lo + per);

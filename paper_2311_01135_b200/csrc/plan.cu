@@ -24,7 +24,7 @@ void launch_enn(const DevBatch &b, cudaStream_t s);
 void launch_onee(const DevBatch &b, cudaStream_t s);
 void launch_grid(const DevBatch &b, int max_atoms, cudaStream_t s);
 void launch_jk(const DevBatch &b, int nmax, cudaStream_t s);
-void launch_xc(const DevBatch &b, int nmax, int nsh_max, cudaStream_t s);
+int launch_xc(const DevBatch &b, const int *bucket_ctas, const int *bucket_n, int nsh_max, cudaStream_t s);
 void launch_orth(const DevBatch &b, cudaStream_t s);
 void launch_post(const DevBatch &b, int it, int diis_start, int diis_hist, double damping, double conv_std,
                  cudaStream_t s);
@@ -64,6 +64,8 @@ struct dftb_plan {
     std::vector<int> nao, nocc, jkc0, xcc0;
     std::vector<int64_t> mat0, npp0, grid0;
     int64_t launches = 0;
+    int *xc_bucket_ctas = nullptr;  // device
+    int xc_bucket_n[6] = {0};
     bool timing = false;
     cudaEvent_t ev[8] = {nullptr};
     double stage_ms[8] = {0};
@@ -201,7 +203,7 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
         const int64_t N = p->nao[m], npp = N * (N + 1) / 2;
         p->mat0[m + 1] = p->mat0[m] + N * N;
         p->npp0[m + 1] = p->npp0[m] + npp;
-        eri0[m + 1] = eri0[m] + npp * (npp + 1) / 2;
+        eri0[m + 1] = eri0[m] + rowbase(npp, opts->precision ? 4 : 2);
         G0[m + 1] = G0[m] + N * (N + 1) / 2 * N;
         const int ncj = (int)((N + 1) / 2);
         for (int c = 0; c < ncj; ++c) {
@@ -224,6 +226,14 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
         V0[m + 1] = V0[m] + (int64_t)ncx * N * N;
     }
     p->grid0[nm] = a_grid0[in->n_atom];
+    // XC CTAs grouped by AO-count bucket (NQ = 4 * ceil(N / 16))
+    std::vector<int> xc_sorted;
+    for (int bkt = 0; bkt < 6; ++bkt) {
+        for (int c = 0; c < (int)xc_mol.size(); ++c)
+            if ((p->nao[xc_mol[c]] + 15) / 16 - 1 == bkt) xc_sorted.push_back(c);
+        p->xc_bucket_n[bkt] = (int)xc_sorted.size() - (bkt ? 0 : 0);
+    }
+    for (int bkt = 5; bkt > 0; --bkt) p->xc_bucket_n[bkt] -= p->xc_bucket_n[bkt - 1];
     const int64_t npts_tot = a_grid0[in->n_atom];
     const int njk = (int)jk_mol.size(), nxc = (int)xc_mol.size();
     const int64_t mat = p->mat0[nm];
@@ -279,6 +289,7 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
     UP(xc_mol, int, xc_mol.data(), nxc)
     UP(xc_p0, int64_t, xc_p0.data(), nxc)
     UP(xc_p1, int64_t, xc_p1.data(), nxc)
+    UP(xc_sorted, int, xc_sorted.data(), nxc)
 #undef UP
     p->in_bytes = (L.off + 255) & ~(size_t)255;
     p->work_off = L.add<char>(0);
@@ -302,6 +313,7 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
     const size_t o_comp = L.add<double>(5 * (size_t)nm);
     const size_t o_Bmat = L.add<double>((size_t)nm * DIIS_MAX * DIIS_MAX);
     const size_t o_eps = L.add<double>((size_t)nm * NMAX);
+    const size_t o_dbg = L.add<long long>((size_t)nm * 16);
     size_t o_ints[7];
     for (int k = 0; k < 7; ++k) o_ints[k] = L.add<int>(nm);
     const int esz = opts->precision ? 4 : 8;
@@ -346,6 +358,7 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
     d.jk_mol = PTR(int, o_jk_mol); d.jk_i0 = PTR(int, o_jk_i0); d.jk_i1 = PTR(int, o_jk_i1); d.n_jk_cta = njk;
     d.xc_mol = PTR(int, o_xc_mol); d.xc_p0 = PTR(int64_t, o_xc_p0); d.xc_p1 = PTR(int64_t, o_xc_p1);
     d.n_xc_cta = nxc;
+    p->xc_bucket_ctas = PTR(int, o_xc_sorted);
     d.g_xyz = PTR(double, o_gxyz); d.g_w = PTR(double, o_gw);
     double **mats[14] = {&d.S, &d.T, &d.V, &d.H, &d.X, &d.C, &d.Cp, &d.rho, &d.rho_prev, &d.F, &d.J, &d.K, &d.Vxc,
                          &d.scratch};
@@ -359,6 +372,7 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
     d.done = PTR(int, o_ints[3]); d.conv = PTR(int, o_ints[4]); d.iters = PTR(int, o_ints[5]);
     d.status = PTR(int, o_ints[6]);
     d.max_it = maxit;
+    d.dbg = PTR(long long, o_dbg);
 #undef PTR
     const double *boys = nullptr;
     int rc = ensure_boys(p->device, &boys);
@@ -427,9 +441,9 @@ int dftb_plan_iterate(dftb_plan *p, int32_t it, void *stream) {
     const DevBatch &d = p->d;
     const dftb_opts &o = p->opts;
     launch_jk(d, p->nmax, st);
-    launch_xc(d, p->nmax, p->nsh_max, st);
+    const int nxl = launch_xc(d, p->xc_bucket_ctas, p->xc_bucket_n, p->nsh_max, st);
     launch_post(d, it, o.diis_start, o.diis_history, o.damping_factor, o.convergence_std, st);
-    p->launches += 2 + (d.n_xc_cta ? 1 : 0);
+    p->launches += 2 + nxl;
     CK(cudaGetLastError());
     return 0;
 }
@@ -464,13 +478,10 @@ int dftb_plan_eri_load(dftb_plan *p, int32_t mol, int64_t count, const uint16_t 
     if (!p || mol < 0 || mol >= p->d.n_mol) return fail(DFTB_EINVAL, "bad arguments");
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t npp = p->npp0[mol + 1] - p->npp0[mol];
-    const int64_t n = npp * (npp + 1) / 2;
+    const int esz = p->d.prec ? 4 : 8, g = 16 / esz;
+    const int64_t n = rowbase(npp, g);
     int64_t e0 = 0;
-    for (int m = 0; m < mol; ++m) {
-        const int64_t q = p->npp0[m + 1] - p->npp0[m];
-        e0 += q * (q + 1) / 2;
-    }
-    const int esz = p->d.prec ? 4 : 8;
+    for (int m = 0; m < mol; ++m) e0 += rowbase(p->npp0[m + 1] - p->npp0[m], g);
     std::vector<unsigned char> host((size_t)n * esz, 0);
     for (int64_t e = 0; e < count; ++e) {
         int64_t P = (int64_t)i[e] * (i[e] + 1) / 2 + j[e], Q = (int64_t)k[e] * (k[e] + 1) / 2 + l[e];
@@ -478,7 +489,7 @@ int dftb_plan_eri_load(dftb_plan *p, int32_t mol, int64_t count, const uint16_t 
         if (k[e] < l[e]) Q = (int64_t)l[e] * (l[e] + 1) / 2 + k[e];
         if (P < Q) std::swap(P, Q);
         if (P >= npp) return fail(DFTB_EINVAL, "index out of range for n_ao");
-        const int64_t off = P * (P + 1) / 2 + Q;
+        const int64_t off = rowbase(P, g) + Q;
         if (esz == 8) reinterpret_cast<double *>(host.data())[off] = v[e];
         else reinterpret_cast<float *>(host.data())[off] = (float)v[e];
     }
@@ -616,7 +627,7 @@ int dftb_plan_xc(dftb_plan *p, const double *rho_host, double *Vxc_host, double 
     cudaStream_t st = (cudaStream_t)stream;
     int rc = upload_rho(p, rho_host, st);
     if (rc) return rc;
-    launch_xc(p->d, p->nmax, p->nsh_max, st);
+    launch_xc(p->d, p->xc_bucket_ctas, p->xc_bucket_n, p->nsh_max, st);
     launch_reduce(p->d, 2, st);
     CK(cudaGetLastError());
     if (Vxc_host) CK(cudaMemcpyAsync(Vxc_host, p->d.Vxc, sizeof(double) * p->mat0[p->d.n_mol], cudaMemcpyDeviceToHost, st));
@@ -732,24 +743,25 @@ int dftb_plan_get(dftb_plan *p, const char *which, int32_t mol, double *host, in
     else if (w == "points") { src = d.g_xyz + 3 * p->grid0[mol]; cnt = 3 * (p->grid0[mol + 1] - p->grid0[mol]); }
     else if (w == "weights") { src = d.g_w + p->grid0[mol]; cnt = p->grid0[mol + 1] - p->grid0[mol]; }
     else if (w == "enn") { src = d.enn + mol; cnt = 1; }
+    else if (w == "dbg") { src = (const double *)(d.dbg + 16 * mol); cnt = 16; }
     else if (w == "eri") {
+        // returned unpadded, in canonical composite order (row P, Q <= P)
         const int64_t npp = p->npp0[mol + 1] - p->npp0[mol];
+        const int esz = d.prec ? 4 : 8, g = 16 / esz;
         cnt = npp * (npp + 1) / 2;
         if (n < cnt) return fail(DFTB_EINVAL, "host buffer too small");
         int64_t e0 = 0;
-        for (int m = 0; m < mol; ++m) {
-            const int64_t q = p->npp0[m + 1] - p->npp0[m];
-            e0 += q * (q + 1) / 2;
-        }
-        if (d.prec == 0) {
-            CK(cudaMemcpyAsync(host, (double *)d.eri + e0, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st));
-        } else {
-            std::vector<float> tmp(cnt);
-            CK(cudaMemcpyAsync(tmp.data(), (float *)d.eri + e0, sizeof(float) * cnt, cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            for (int64_t k = 0; k < cnt; ++k) host[k] = tmp[k];
-        }
+        for (int m = 0; m < mol; ++m) e0 += rowbase(p->npp0[m + 1] - p->npp0[m], g);
+        const int64_t padded = rowbase(npp, g);
+        std::vector<unsigned char> tmp((size_t)padded * esz);
+        CK(cudaMemcpyAsync(tmp.data(), (unsigned char *)d.eri + (size_t)e0 * esz, tmp.size(), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+        for (int64_t P = 0; P < npp; ++P)
+            for (int64_t Q = 0; Q <= P; ++Q) {
+                const int64_t src = rowbase(P, g) + Q;
+                host[P * (P + 1) / 2 + Q] = esz == 8 ? reinterpret_cast<double *>(tmp.data())[src]
+                                                     : (double)reinterpret_cast<float *>(tmp.data())[src];
+            }
         return 0;
     } else {
         return fail(DFTB_EINVAL, "unknown buffer " + w);

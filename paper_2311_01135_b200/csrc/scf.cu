@@ -17,10 +17,11 @@ constexpr int SCF_THREADS = 512;
 constexpr int KP = 32;  // GEMM K-panel
 
 struct Arena {
-    double *A, *B;      // NMAX*NMAX each
-    double *sa, *sb;    // KP*NMAX each (GEMM staging)
-    double *cs, *sn;    // rotations [NMAX/2+1]
-    int *pp, *qq;       // rotation pairs
+    double *A, *B, *W;  // NMAX*NMAX each; W doubles as GEMM staging and Jacobi's second A buffer
+    double *sa, *sb;    // KP*NMAX each, inside W
+    double *cs, *sn;    // rotations, double-buffered [2][NMAX/2+1]
+    int *pp, *qq;       // rotation pairs [2][NMAX/2+1]
+    int *pos;           // index -> 2*pair + is_q, [2][NMAX+2]
     int *perm;          // [NMAX]
     double *dv;         // [NMAX]
     double *Bs;         // [10*10] DIIS system
@@ -29,30 +30,34 @@ struct Arena {
     double *scal;       // [16] scalars broadcast
 };
 
+constexpr int NPH = NMAX / 2 + 1;
+
 __device__ __forceinline__ Arena carve(unsigned char *base) {
     Arena a;
     double *p = (double *)base;
     a.A = p; p += NMAX * NMAX;
     a.B = p; p += NMAX * NMAX;
-    a.sa = p; p += KP * NMAX;
-    a.sb = p; p += KP * NMAX;
-    a.cs = p; p += NMAX / 2 + 2;
-    a.sn = p; p += NMAX / 2 + 2;
+    a.W = p; p += NMAX * NMAX;
+    a.sa = a.W;
+    a.sb = a.W + KP * NMAX;
+    a.cs = p; p += 2 * NPH;
+    a.sn = p; p += 2 * NPH;
     a.dv = p; p += NMAX;
     a.Bs = p; p += 100;
     a.cf = p; p += 10;
     a.red = p; p += 32;
     a.scal = p; p += 16;
     int *q = (int *)p;
-    a.pp = q; q += NMAX / 2 + 2;
-    a.qq = q; q += NMAX / 2 + 2;
+    a.pp = q; q += 2 * NPH;
+    a.qq = q; q += 2 * NPH;
+    a.pos = q; q += 2 * (NMAX + 2);
     a.perm = q; q += NMAX;
     return a;
 }
 
 size_t scf_smem_bytes() {
-    return sizeof(double) * (2 * NMAX * NMAX + 2 * KP * NMAX + 2 * (NMAX / 2 + 2) + NMAX + 100 + 10 + 32 + 16) +
-           sizeof(int) * (2 * (NMAX / 2 + 2) + NMAX);
+    return sizeof(double) * (3 * NMAX * NMAX + 4 * NPH + NMAX + 100 + 10 + 32 + 16) +
+           sizeof(int) * (4 * NPH + 2 * (NMAX + 2) + NMAX);
 }
 
 // C (M x N, ldc) = alpha * op(A) op(B) + beta * C ; op(A) is M x K, op(B) is K x N.
@@ -67,16 +72,20 @@ __device__ void cta_gemm(double *C, int ldc, const double *A, int lda, bool tA, 
         for (int c = 0; c < 3; ++c) acc[a][c] = 0.0;
     for (int k0 = 0; k0 < K; k0 += KP) {
         const int kn = min(KP, K - k0);
+        // staging loops map consecutive threads to the operand's contiguous index (coalesced)
         for (int t = tid; t < KP * NMAX; t += SCF_THREADS) {
-            const int kk = t / NMAX, i = t % NMAX;
-            double va = 0.0, vb = 0.0;
-            if (kk < kn) {
-                const int k = k0 + kk;
-                if (i < M) va = tA ? A[(int64_t)k * lda + i] : A[(int64_t)i * lda + k];
-                if (i < N) vb = tB ? B[(int64_t)i * ldb + k] : B[(int64_t)k * ldb + i];
-            }
-            ar.sa[t] = va;
-            ar.sb[t] = vb;
+            int kk, i;
+            if (tA) { kk = t / NMAX; i = t % NMAX; } else { i = t / KP; kk = t % KP; }
+            double va = 0.0;
+            if (kk < kn && i < M) va = tA ? A[(int64_t)(k0 + kk) * lda + i] : A[(int64_t)i * lda + k0 + kk];
+            ar.sa[kk * NMAX + i] = va;
+        }
+        for (int t = tid; t < KP * NMAX; t += SCF_THREADS) {
+            int kk, j;
+            if (!tB) { kk = t / NMAX; j = t % NMAX; } else { j = t / KP; kk = t % KP; }
+            double vb = 0.0;
+            if (kk < kn && j < N) vb = tB ? B[(int64_t)j * ldb + k0 + kk] : B[(int64_t)(k0 + kk) * ldb + j];
+            ar.sb[kk * NMAX + j] = vb;
         }
         __syncthreads();
         for (int kk = 0; kk < kn; ++kk) {
@@ -106,67 +115,136 @@ __device__ void cta_gemm(double *C, int ldc, const double *A, int lda, bool tA, 
     __syncthreads();
 }
 
-// Cyclic Jacobi with the round-robin (circle) ordering: n/2 disjoint rotations per
-// step, rows then columns.  A (n x n, ld n) -> diagonal; V accumulates rotations.
-__device__ void cta_jacobi(double *A, double *V, int n, const Arena &ar, int max_sweeps = 40) {
-    const int tid = threadIdx.x, nt = SCF_THREADS;
-    const int n2 = n + (n & 1), np = n2 / 2;
-    for (int sweep = 0; sweep < max_sweeps; ++sweep) {
-        double off = 0.0, dg = 0.0;
-        for (int t = tid; t < n * n; t += nt) {
-            const int p = t / n, q = t % n;
-            if (q > p) off = fmax(off, fabs(A[t]));
-            else if (q == p) dg = fmax(dg, fabs(A[t]));
-        }
-        off = block_max(off, ar.red);
-        dg = block_max(dg, ar.red);
-        if (off <= 1e-15 * dg || off < 1e-300) break;
-        for (int r = 0; r < n2 - 1; ++r) {
-            if (tid < np) {
-                int p, q;
-                if (tid == 0) { p = r; q = n2 - 1; }
-                else { p = (r + tid) % (n2 - 1); q = (r - tid + n2 - 1) % (n2 - 1); }
-                if (p > q) { int t = p; p = q; q = t; }
-                double c = 1.0, s = 0.0;
-                if (q < n) {
-                    const double apq = A[p * n + q];
-                    if (fabs(apq) > 1e-300) {
-                        const double th = (A[q * n + q] - A[p * n + p]) / (2.0 * apq);
-                        const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
-                        c = 1.0 / sqrt(t * t + 1.0);
-                        s = t * c;
-                    }
-                }
-                ar.cs[tid] = c; ar.sn[tid] = s; ar.pp[tid] = p; ar.qq[tid] = q;
-            }
-            __syncthreads();
-            for (int t = tid; t < np * n; t += nt) {
-                const int k = t / n, col = t % n;
-                const double s = ar.sn[k];
-                if (s == 0.0) continue;
-                const double c = ar.cs[k];
-                const int p = ar.pp[k], q = ar.qq[k];
-                const double ap = A[p * n + col], aq = A[q * n + col];
-                A[p * n + col] = c * ap - s * aq;
-                A[q * n + col] = s * ap + c * aq;
-            }
-            __syncthreads();
-            for (int t = tid; t < np * n; t += nt) {
-                const int k = t / n, row = t % n;
-                const double s = ar.sn[k];
-                if (s == 0.0) continue;
-                const double c = ar.cs[k];
-                const int p = ar.pp[k], q = ar.qq[k];
-                const double ap = A[row * n + p], aq = A[row * n + q];
-                A[row * n + p] = c * ap - s * aq;
-                A[row * n + q] = s * ap + c * aq;
-                const double vp = V[row * n + p], vq = V[row * n + q];
-                V[row * n + p] = c * vp - s * vq;
-                V[row * n + q] = s * vp + c * vq;
-            }
-            __syncthreads();
-        }
+// Cyclic Jacobi, round-robin (circle) pairing: n/2 disjoint rotations per step,
+// applied at once as J^T A J on 2x2 blocks (rows of pair k1 x columns of pair k2)
+// from buffer `cur` into buffer `nxt`, V <- V J in place.  The angles of step r+1
+// are computed in the SAME pass from cur and the step-r rotations (each needs only
+// three transformed elements), so a step costs one CTA barrier.
+// Returns the buffer holding the converged (diagonal) matrix; *nsweeps = sweeps.
+constexpr int JAC_MAXT = (NPH * NPH + NMAX * NPH + SCF_THREADS - 1) / SCF_THREADS;
+
+__device__ __forceinline__ void jac_pair(int k, int r, int n2, int &p, int &q) {
+    if (k == 0) { p = r; q = n2 - 1; }
+    else { p = (r + k) % (n2 - 1); q = (r - k + n2 - 1) % (n2 - 1); }
+    if (p > q) { int t = p; p = q; q = t; }
+}
+
+__device__ __forceinline__ void jac_angle(double app, double aqq, double apq, double &c, double &s) {
+    c = 1.0;
+    s = 0.0;
+    if (fabs(apq) > 1e-300 && fabs(apq) > 1e-17 * (fabs(app) + fabs(aqq))) {
+        const double th = (aqq - app) / (2.0 * apq);
+        const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+        c = rsqrt(t * t + 1.0);
+        s = t * c;
     }
+}
+
+__device__ double *cta_jacobi(double *A0, double *A1, double *V, int n, const Arena &ar, int *nsweeps,
+                              int max_sweeps = 30) {
+    const int tid = threadIdx.x, nt = SCF_THREADS;
+    const int n2 = n + (n & 1), np = n2 / 2, R = n2 - 1;
+    const int nblk = np * np, ntask = nblk + n * np;
+    int task[JAC_MAXT];
+#pragma unroll
+    for (int s = 0; s < JAC_MAXT; ++s) {
+        const int t = tid + s * nt;
+        if (t < nblk) task[s] = ((t / np) << 16) | (t % np);
+        else if (t < ntask) task[s] = (((t - nblk) / np) << 16) | ((t - nblk) % np);
+        else task[s] = -1;
+    }
+    double *cur = A0, *nxt = A1;
+    // rotations of global step 0 from cur directly (buffer 0)
+    if (tid < np) {
+        int p, q;
+        jac_pair(tid, 0, n2, p, q);
+        double c = 1.0, sn = 0.0;
+        if (q < n) jac_angle(cur[p * n + p], cur[q * n + q], cur[p * n + q], c, sn);
+        ar.cs[tid] = c; ar.sn[tid] = sn; ar.pp[tid] = p; ar.qq[tid] = q;
+        ar.pos[p] = 2 * tid; ar.pos[q] = 2 * tid + 1;
+    }
+    __syncthreads();
+    int sweeps = 0;
+    for (int g = 0;; ++g) {
+        const int r = g % R, bf = g & 1, nb = bf ^ 1;
+        if (r == 0) {
+            double off = 0.0, dg = 0.0;
+            for (int t = tid; t < n * n; t += nt) {
+                const int p = t / n, q = t - p * n;
+                const double a = fabs(cur[t]);
+                if (q > p) {
+                    if (a > 1e-15 * sqrt(fabs(cur[p * n + p] * cur[q * n + q]))) off = fmax(off, a);
+                } else if (q == p) {
+                    dg = fmax(dg, a);
+                }
+            }
+            off = block_max(off, ar.red);
+            dg = block_max(dg, ar.red);
+            if (off <= 1e-13 * dg || off < 1e-300 || sweeps >= max_sweeps) break;
+            ++sweeps;
+        }
+        const double *cs = ar.cs + bf * NPH, *sn = ar.sn + bf * NPH;
+        const int *pp = ar.pp + bf * NPH, *qq = ar.qq + bf * NPH, *pos = ar.pos + bf * (NMAX + 2);
+        if (tid < np) {  // angles for step g+1 from cur and this step's rotations
+            const int r1 = (g + 1) % R;
+            int p, q;
+            jac_pair(tid, r1, n2, p, q);
+            double c = 1.0, s1 = 0.0;
+            if (q < n) {
+                // element (x, y) of J^T cur J
+                auto el = [&](int x, int y) {
+                    const int kx = pos[x] >> 1, ky = pos[y] >> 1;
+                    const double cx = cs[kx], sx = sn[kx], cy = cs[ky], sy = sn[ky];
+                    const int px = pp[kx], qx = qq[kx], py = pp[ky], qy = qq[ky];
+                    const double la = (pos[x] & 1) ? sx : cx, lb = (pos[x] & 1) ? cx : -sx;
+                    const double ra = (pos[y] & 1) ? sy : cy, rb = (pos[y] & 1) ? cy : -sy;
+                    const bool hx = qx < n && lb != 0.0, hy = qy < n && rb != 0.0;
+                    double v = la * ra * cur[px * n + py];
+                    if (hy) v += la * rb * cur[px * n + qy];
+                    if (hx) v += lb * ra * cur[qx * n + py];
+                    if (hx && hy) v += lb * rb * cur[qx * n + qy];
+                    return v;
+                };
+                jac_angle(el(p, p), el(q, q), el(p, q), c, s1);
+            }
+            ar.cs[nb * NPH + tid] = c; ar.sn[nb * NPH + tid] = s1;
+            ar.pp[nb * NPH + tid] = p; ar.qq[nb * NPH + tid] = q;
+            ar.pos[nb * (NMAX + 2) + p] = 2 * tid; ar.pos[nb * (NMAX + 2) + q] = 2 * tid + 1;
+        }
+#pragma unroll
+        for (int s = 0; s < JAC_MAXT; ++s) {
+            const int t = tid + s * nt;
+            if (t >= ntask) break;
+            const int u = task[s] >> 16, v = task[s] & 0xffff;
+            if (t < nblk) {
+                const double s1 = sn[u], s2 = sn[v], c1 = cs[u], c2 = cs[v];
+                const int p1 = pp[u], q1 = qq[u], p2 = pp[v], q2 = qq[v];
+                const bool hq1 = q1 < n, hq2 = q2 < n;
+                const double xpp = cur[p1 * n + p2];
+                const double xpq = hq2 ? cur[p1 * n + q2] : 0.0;
+                const double xqp = hq1 ? cur[q1 * n + p2] : 0.0;
+                const double xqq = (hq1 && hq2) ? cur[q1 * n + q2] : 0.0;
+                const double ypp = c1 * xpp - s1 * xqp, yqp = s1 * xpp + c1 * xqp;
+                const double ypq = c1 * xpq - s1 * xqq, yqq = s1 * xpq + c1 * xqq;
+                nxt[p1 * n + p2] = c2 * ypp - s2 * ypq;
+                if (hq2) nxt[p1 * n + q2] = s2 * ypp + c2 * ypq;
+                if (hq1) nxt[q1 * n + p2] = c2 * yqp - s2 * yqq;
+                if (hq1 && hq2) nxt[q1 * n + q2] = s2 * yqp + c2 * yqq;
+            } else {
+                const double sv = sn[v];
+                if (sv == 0.0) continue;
+                const double cv = cs[v];
+                const int p = pp[v], q = qq[v];
+                const double vp = V[u * n + p], vq = V[u * n + q];
+                V[u * n + p] = cv * vp - sv * vq;
+                V[u * n + q] = sv * vp + cv * vq;
+            }
+        }
+        __syncthreads();
+        double *t = cur; cur = nxt; nxt = t;
+    }
+    *nsweeps = sweeps;
+    return cur;
 }
 
 // ascending order of diag(A) -> ar.perm (rank of each original index), stable by index
@@ -196,8 +274,11 @@ __global__ void __launch_bounds__(SCF_THREADS) k_orth(DevBatch b) {
         ar.B[t] = (t / N == t % N) ? 1.0 : 0.0;
     }
     __syncthreads();
-    cta_jacobi(ar.A, ar.B, N, ar);
-    sort_eigs(ar.A, N, ar);
+    const long long t0 = clock64();
+    int nsw = 0;
+    const double *Ad = cta_jacobi(ar.A, ar.W, ar.B, N, ar, &nsw);
+    if (b.dbg && tid == 0) { b.dbg[16 * m + 12] = clock64() - t0; b.dbg[16 * m + 13] = nsw; }
+    sort_eigs(Ad, N, ar);
     // kept = s > 1e-7, in ascending order: sorted positions [N - M, N)
     if (tid == 0) {
         int M = 0;
@@ -337,11 +418,12 @@ __device__ void diis_extrapolate(const DevBatch &b, int m, int N, const double *
         ar.B[t] = (r == c) ? 1.0 : 0.0;
     }
     __syncthreads();
-    cta_jacobi(ar.A, ar.B, n1, ar);
+    int nsw1 = 0;
+    const double *Ad = cta_jacobi(ar.A, ar.W, ar.B, n1, ar, &nsw1);
     if (tid == 0) {
         double mx = 0.0, mn = 1e308;
         for (int i = 0; i < n1; ++i) {
-            const double e = fabs(ar.A[i * n1 + i]);
+            const double e = fabs(Ad[i * n1 + i]);
             mx = fmax(mx, e);
             mn = fmin(mn, e);
         }
@@ -402,10 +484,14 @@ __global__ void __launch_bounds__(SCF_THREADS) k_post(DevBatch b, PostArgs pa) {
     double *S1 = b.scratch + o, *S2 = b.scratch + tot + o;
     const int it = pa.it;
     const double *Fuse = H;
+    long long t0 = clock64(), tl = t0;
+    long long *dbg = b.dbg ? b.dbg + 16 * m : nullptr;
+    auto tick = [&](int k) { if (dbg && tid == 0) { long long t = clock64(); dbg[k] += t - tl; tl = t; } };
     if (it >= 0) {
         reduce_jk(b, m, N, J, K);
         reduce_vxc(b, m, N, Vx);
         __syncthreads();
+        tick(0);
         // (4) F and (5) energies
         double ec = 0.0, ej = 0.0, ek = 0.0;
         for (int t = tid; t < N * N; t += SCF_THREADS) {
@@ -428,6 +514,7 @@ __global__ void __launch_bounds__(SCF_THREADS) k_post(DevBatch b, PostArgs pa) {
             cp[4] = exc;
             b.hist[(int64_t)m * b.max_it + it] = cp[0] + cp[1] + cp[2] + cp[3] + cp[4];
         }
+        tick(1);
         // (6) DIIS error e = F rho S - S rho F = A - A^T with A = F rho S
         cta_gemm(S1, N, F, N, false, rho, N, false, N, N, N, 1.0, 0.0, ar);
         cta_gemm(S2, N, S1, N, false, S, N, false, N, N, N, 1.0, 0.0, ar);
@@ -459,6 +546,7 @@ __global__ void __launch_bounds__(SCF_THREADS) k_post(DevBatch b, PostArgs pa) {
             b.ring_n[m] = nh_new;
         }
         __syncthreads();
+        tick(2);
         // (8) extrapolation
         if (it + 1 >= pa.diis_start) {
             diis_extrapolate(b, m, N, F, S1, pa, ar);
@@ -467,6 +555,7 @@ __global__ void __launch_bounds__(SCF_THREADS) k_post(DevBatch b, PostArgs pa) {
             Fuse = F;
         }
     }
+    tick(3);
     // (9) Roothaan: F' = X^T F X, Jacobi (warm start from previous C'), C = X C'
     cta_gemm(S2, N, Fuse, N, false, X, N, false, N, M, N, 1.0, 0.0, ar);     // F X  (N x M, ld N)
     cta_gemm(ar.A, M, X, N, true, S2, N, false, M, M, N, 1.0, 0.0, ar);      // X^T (F X)
@@ -478,8 +567,12 @@ __global__ void __launch_bounds__(SCF_THREADS) k_post(DevBatch b, PostArgs pa) {
         for (int t = tid; t < M * M; t += SCF_THREADS) ar.B[t] = (t / M == t % M) ? 1.0 : 0.0;
     }
     __syncthreads();
-    cta_jacobi(ar.A, ar.B, M, ar);
-    sort_eigs(ar.A, M, ar);
+    tick(4);
+    int nsw = 0;
+    const double *Ad = cta_jacobi(ar.A, ar.W, ar.B, M, ar, &nsw);
+    if (dbg && tid == 0) dbg[10] += nsw;
+    tick(5);
+    sort_eigs(Ad, M, ar);
     for (int t = tid; t < M * M; t += SCF_THREADS) {
         const int row = t / M, i = t % M;
         Cp[row * M + ar.perm[i]] = ar.B[t];
@@ -498,6 +591,8 @@ __global__ void __launch_bounds__(SCF_THREADS) k_post(DevBatch b, PostArgs pa) {
         if (b.prec) v = (double)(float)v;
         rho[t] = v;
     }
+    tick(6);
+    if (dbg && tid == 0) dbg[11] += 1;
     if (tid == 0 && it >= 0) {
         b.iters[m] = it + 1;
         bool stop = (it + 1 >= b.max_it);
@@ -544,8 +639,9 @@ __global__ void __launch_bounds__(SCF_THREADS) k_roothaan(DevBatch b) {
     cta_gemm(ar.A, M, X, N, true, S2, N, false, M, M, N, 1.0, 0.0, ar);
     for (int t = tid; t < M * M; t += SCF_THREADS) ar.B[t] = (t / M == t % M) ? 1.0 : 0.0;
     __syncthreads();
-    cta_jacobi(ar.A, ar.B, M, ar);
-    sort_eigs(ar.A, M, ar);
+    int nsw = 0;
+    const double *Ad = cta_jacobi(ar.A, ar.W, ar.B, M, ar, &nsw);
+    sort_eigs(Ad, M, ar);
     for (int t = tid; t < M * M; t += SCF_THREADS) Cp[(t / M) * M + ar.perm[t % M]] = ar.B[t];
     for (int i = tid; i < M; i += SCF_THREADS) b.eps[(int64_t)m * NMAX + ar.perm[i]] = ar.dv[i];
     __syncthreads();
@@ -588,10 +684,11 @@ __global__ void __launch_bounds__(SCF_THREADS) k_diis_single(const double *F, co
         ar.B[t] = (t / n1 == t % n1) ? 1.0 : 0.0;
     }
     __syncthreads();
-    cta_jacobi(ar.A, ar.B, n1, ar);
+    int nsw2 = 0;
+    const double *Ad = cta_jacobi(ar.A, ar.W, ar.B, n1, ar, &nsw2);
     if (tid == 0) {
         double mx = 0.0, mn = 1e308;
-        for (int i = 0; i < n1; ++i) { const double e = fabs(ar.A[i * n1 + i]); mx = fmax(mx, e); mn = fmin(mn, e); }
+        for (int i = 0; i < n1; ++i) { const double e = fabs(Ad[i * n1 + i]); mx = fmax(mx, e); mn = fmin(mn, e); }
         const bool fb = !(mn > 0.0) || (mx / mn > 1e12);
         ar.scal[1] = fb;
         if (!fb) {

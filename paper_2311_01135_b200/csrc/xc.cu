@@ -5,271 +5,345 @@
 // grad phi for the whole grid and runs two BLAS GEMMs per 8192-point batch.
 //
 // B200 formulation: one CTA owns a contiguous range of one molecule's grid
-// points.  AO values and gradients are recomputed per 32-point sub-block into
-// shared memory (never written to HBM), so each SCF iteration reads only the
-// density matrix and writes one N x N partial per CTA:
-//   pass A: phi -> t = phi rho (smem GEMM) -> n, grad n per point,
-//   pass B: B3LYP per point (one thread per point, f64),
-//   pass C: phi again -> wv = a phi + b . grad phi -> V += phi^T wv (register tiles).
-// W is the arithmetic type of the contractions (double for the f64 build, float for
-// the f32 build, as in the reference's f32 BLAS path); the functional is always f64.
+// points and walks it in BP-point sub-blocks (64 in the f32 build, 32 in f64).
+// Per sub-block the AO values and gradients are evaluated ONCE into shared
+// memory (never written to HBM), stored [AO][point] with a 16-byte-group XOR
+// swizzle so that every access pattern below is bank-conflict free:
+//   t = phi rho and n, grad n   4 points x 4 AOs per thread in registers, 128-bit
+//                               smem loads, partial sums reduced over the lanes
+//                               sharing the points by a shuffle tree;
+//   B3LYP                       one thread per point, f64;
+//   wv = a phi + b . grad phi   elementwise;
+//   V += phi wv^T               4 x 4 register tiles accumulated over the CTA's
+//                               whole point range, written once as a partial.
+// Each SCF iteration reads only rho and writes one N x N partial per CTA.  CTAs
+// are launched per AO-count bucket (NQ = ceil(N/16)*4 quads), so every kernel
+// instance has compile-time tile loops and its own shared-memory footprint.
+// W is the arithmetic type of the contractions: double in the f64 build, float in
+// the f32 build (the reference's f32 BLAS path); the functional is always f64.
 #include "common.cuh"
 #include "b3lyp.cuh"
 
 namespace dftb {
 
 constexpr int XC_THREADS = 256;
-constexpr int XC_SB = 256;       // points per super-block (one per thread in pass B)
 constexpr int XC_SHD = 13;       // doubles per shell record in smem
 
 template <typename W>
-struct XCSmem {
-    W *rho, *phi, *tw;
-    double *pt, *dn, *shd, *red;
+struct Vec4;
+template <>
+struct Vec4<float> {
+    __device__ static __forceinline__ void ld(const float *p, float (&o)[4]) {
+        const float4 v = *reinterpret_cast<const float4 *>(p);
+        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+    }
+};
+template <>
+struct Vec4<double> {
+    __device__ static __forceinline__ void ld(const double *p, double (&o)[4]) {
+        const double2 a = *reinterpret_cast<const double2 *>(p);
+        const double2 b = *reinterpret_cast<const double2 *>(p + 2);
+        o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
+    }
 };
 
-template <typename W>
-__device__ __forceinline__ void xc_eval_phi(const XCSmem<W> &s, int nsh, int NP, int BP, int sub, int nb) {
-    const int plane = BP * NP;
+// physical offset of logical (row, col) in a [rows][BP] tile, col groups of 4 swizzled by row quad
+template <int BP>
+__device__ __forceinline__ int swz(int row, int col) {
+    return row * BP + ((((col >> 2) ^ (row >> 2)) & (BP / 4 - 1)) << 2) + (col & 3);
+}
+
+template <typename W, int NQ, int BP>
+struct XCL {
+    static constexpr int NP = 4 * NQ;
+    static constexpr size_t rho = 0;
+    static constexpr size_t phi = rho + sizeof(W) * NP * NP;
+    static constexpr size_t wv = phi + sizeof(W) * 4 * NP * BP;
+    static constexpr size_t pt = wv + sizeof(W) * NP * BP;
+    static constexpr size_t dn = pt + sizeof(double) * 4 * BP;
+    static constexpr size_t red = dn + sizeof(double) * 4 * BP;
+    static constexpr size_t shd = red + sizeof(double) * 32;
+    static size_t bytes(int nsh) { return shd + sizeof(double) * XC_SHD * (size_t)nsh; }
+};
+
+template <typename W, int NQ, int BP>
+__device__ __forceinline__ void xc_eval_phi(W *phi, const double *pt, const double *shd, int nsh, int nb) {
+    constexpr int NP = 4 * NQ, PL = NP * BP;
     for (int t = threadIdx.x; t < BP * nsh; t += XC_THREADS) {
         const int p = t % BP, sh = t / BP;
-        const double *r = s.shd + XC_SHD * sh;
+        const double *r = shd + XC_SHD * sh;
         const int kind = (int)r[12] & 1, ao = (int)r[12] >> 1;
-        W *o0 = s.phi + p * NP + ao;
-        if (p >= nb) {
-            const int nc = kind ? 4 : 1;
-            for (int c = 0; c < nc; ++c) o0[c] = o0[plane + c] = o0[2 * plane + c] = o0[3 * plane + c] = (W)0;
-            continue;
-        }
-        const double *q = s.pt + 4 * (sub + p);
-        const double dx = q[0] - r[0], dy = q[1] - r[1], dz = q[2] - r[2];
-        const double r2 = dx * dx + dy * dy + dz * dz;
-        double bs = 0.0, ds = 0.0, bp = 0.0, dp = 0.0;
+        W v[4][4];  // [plane][component]
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            const double ar = r[3 + k] * r2;
-            const double e = ar < 745.0 ? exp(-ar) : 0.0;
-            const double m2a = -2.0 * r[3 + k];
-            bs += r[6 + k] * e;
-            ds += r[6 + k] * m2a * e;
-            bp += r[9 + k] * e;
-            dp += r[9 + k] * m2a * e;
-        }
-        o0[0] = (W)bs;
-        o0[plane] = (W)(dx * ds);
-        o0[2 * plane] = (W)(dy * ds);
-        o0[3 * plane] = (W)(dz * ds);
-        if (kind) {
-            const double rel[3] = {dx, dy, dz};
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) v[a][c] = (W)0;
+        if (p < nb) {
+            const double *q = pt + 4 * p;
+            const W dx = (W)(q[0] - r[0]), dy = (W)(q[1] - r[1]), dz = (W)(q[2] - r[2]);
+            const W r2 = dx * dx + dy * dy + dz * dz;
+            W bs = 0, ds = 0, bp = 0, dp = 0;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const W a = (W)r[3 + k];
+                const W ar = a * r2;
+                W e;
+                if constexpr (sizeof(W) == 4) e = ar < (W)88 ? expf(-ar) : (W)0;
+                else e = ar < (W)745 ? exp(-ar) : (W)0;
+                const W m2a = (W)-2 * a;
+                bs += (W)r[6 + k] * e;
+                ds += (W)r[6 + k] * m2a * e;
+                bp += (W)r[9 + k] * e;
+                dp += (W)r[9 + k] * m2a * e;
+            }
+            const W rel[3] = {dx, dy, dz};
+            v[0][0] = bs;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) v[d + 1][0] = rel[d] * ds;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                o0[1 + c] = (W)(rel[c] * bp);
+                v[0][1 + c] = rel[c] * bp;
 #pragma unroll
-                for (int d = 0; d < 3; ++d)
-                    o0[(d + 1) * plane + 1 + c] = (W)((c == d ? bp : 0.0) + rel[c] * rel[d] * dp);
+                for (int d = 0; d < 3; ++d) v[d + 1][1 + c] = (c == d ? bp : (W)0) + rel[c] * rel[d] * dp;
             }
+        }
+        const int nc = kind ? 4 : 1;
+        for (int c = 0; c < nc; ++c) {
+            const int o = swz<BP>(ao + c, p);
+#pragma unroll
+            for (int a = 0; a < 4; ++a) phi[a * PL + o] = v[a][c];
         }
     }
 }
 
-template <typename W, int BP>
-__global__ void __launch_bounds__(XC_THREADS) k_xc(DevBatch b) {
+template <typename W, int NQ, int BP>
+__global__ void __launch_bounds__(XC_THREADS) k_xc(DevBatch b, const int *ctas) {
+    using L = XCL<W, NQ, BP>;
+    constexpr int NP = 4 * NQ, PL = NP * BP;
+    constexpr int PG = BP / 4;                 // point groups (4 points each)
+    constexpr int LG = XC_THREADS / PG;        // lanes sharing a point group
+    constexpr int QJ = (NQ + LG - 1) / LG;     // column quads per lane in the t phase
+    constexpr int NT = NQ * NQ;                // V tiles (4 x 4)
+    constexpr int TJ = (NT + XC_THREADS - 1) / XC_THREADS;
     extern __shared__ __align__(16) unsigned char xsm[];
-    constexpr int G = XC_THREADS / BP;           // threads per point in the per-point phases
-    const int cta = blockIdx.x;
+    const int cta = ctas[blockIdx.x];
     const int m = b.xc_mol[cta];
     if (b.done[m]) return;
     const int N = b.m_nao[m];
-    const int NP = (N + 15) & ~15;
     const int nsh = b.m_nshell[m], s0 = b.m_shell0[m];
-    XCSmem<W> s;
-    s.rho = (W *)xsm;
-    s.phi = s.rho + NP * NP;
-    s.tw = s.phi + 4 * BP * NP;
-    s.pt = (double *)(s.tw + BP * NP + ((BP * NP) & 1));
-    s.pt = (double *)(((uintptr_t)s.pt + 15) & ~(uintptr_t)15);
-    s.dn = s.pt + 4 * XC_SB;
-    s.shd = s.dn + 4 * XC_SB;
-    s.red = s.shd + XC_SHD * nsh;
+    W *rho = (W *)(xsm + L::rho);
+    W *phi = (W *)(xsm + L::phi);
+    W *wv = (W *)(xsm + L::wv);
+    double *pt = (double *)(xsm + L::pt);
+    double *dn = (double *)(xsm + L::dn);
+    double *red = (double *)(xsm + L::red);
+    double *shd = (double *)(xsm + L::shd);
     const int tid = threadIdx.x;
     const double *rg = b.rho + b.m_mat0[m];
     for (int t = tid; t < NP * NP; t += XC_THREADS) {
         const int r = t / NP, c = t % NP;
-        s.rho[t] = (r < N && c < N) ? (W)rg[r * N + c] : (W)0;
+        rho[t] = (r < N && c < N) ? (W)rg[r * N + c] : (W)0;
     }
-    for (int t = tid; t < 4 * BP * NP; t += XC_THREADS) s.phi[t] = (W)0;
-    for (int t = tid; t < BP * NP; t += XC_THREADS) s.tw[t] = (W)0;
+    for (int t = tid; t < 4 * PL; t += XC_THREADS) phi[t] = (W)0;
     for (int sh = tid; sh < nsh; sh += XC_THREADS) {
-        const int g = s0 + sh;
-        double *r = s.shd + XC_SHD * sh;
-        const double *A = b.a_xyz + 3 * b.s_atom[g];
+        const int gsh = s0 + sh;
+        double *r = shd + XC_SHD * sh;
+        const double *A = b.a_xyz + 3 * b.s_atom[gsh];
         for (int d = 0; d < 3; ++d) {
             r[d] = A[d];
-            r[3 + d] = b.s_exp[3 * g + d];
-            r[6 + d] = b.s_cs[3 * g + d];
-            r[9 + d] = b.s_cp[3 * g + d];
+            r[3 + d] = b.s_exp[3 * gsh + d];
+            r[6 + d] = b.s_cs[3 * gsh + d];
+            r[9 + d] = b.s_cp[3 * gsh + d];
         }
-        r[12] = (double)((b.s_ao[g] << 1) | (b.s_kind[g] & 1));
+        r[12] = (double)((b.s_ao[gsh] << 1) | (b.s_kind[gsh] & 1));
     }
-    // V accumulator tile: rows ty + 16 a, cols tx + 16 c
-    const int ty = tid >> 4, tx = tid & 15;
-    W acc[6][6];
+    W acc[TJ][4][4];
 #pragma unroll
-    for (int a = 0; a < 6; ++a)
+    for (int j = 0; j < TJ; ++j)
 #pragma unroll
-        for (int c = 0; c < 6; ++c) acc[a][c] = (W)0;
-    const int nblk16 = NP >> 4;
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[j][a][c] = (W)0;
     double e_acc = 0.0;
     int bad = 0;
+    const int pg = tid / LG, lg = tid % LG;
     const int64_t p0 = b.xc_p0[cta], p1 = b.xc_p1[cta];
-    const int plane = BP * NP;
-    const int gp = tid / G, gl = tid % G;         // point-group mapping
-    for (int64_t sb0 = p0; sb0 < p1; sb0 += XC_SB) {
-        const int nsb = (int)min((int64_t)XC_SB, p1 - sb0);
-        __syncthreads();
-        if (tid < nsb) {
-            const int64_t gi = sb0 + tid;
-            s.pt[4 * tid] = b.g_xyz[3 * gi];
-            s.pt[4 * tid + 1] = b.g_xyz[3 * gi + 1];
-            s.pt[4 * tid + 2] = b.g_xyz[3 * gi + 2];
-            s.pt[4 * tid + 3] = b.g_w[gi];
+    for (int64_t sb = p0; sb < p1; sb += BP) {
+        const int nb = (int)min((int64_t)BP, p1 - sb);
+        __syncthreads();                                   // previous sub-block consumed
+        if (tid < BP) {
+            const int64_t gi = sb + min(tid, nb - 1);
+            pt[4 * tid] = b.g_xyz[3 * gi];
+            pt[4 * tid + 1] = b.g_xyz[3 * gi + 1];
+            pt[4 * tid + 2] = b.g_xyz[3 * gi + 2];
+            pt[4 * tid + 3] = tid < nb ? b.g_w[gi] : 0.0;
         }
         __syncthreads();
-        // ---- pass A: density and gradient
-        for (int sub = 0; sub < nsb; sub += BP) {
-            const int nb = min(BP, nsb - sub);
-            xc_eval_phi(s, nsh, NP, BP, sub, nb);
-            __syncthreads();
-            {   // t = phi rho : point gp, columns gl + G r
-                W t[96 / G];
+        xc_eval_phi<W, NQ, BP>(phi, pt, shd, nsh, nb);
+        __syncthreads();
+        {   // ---- t = phi^T rho for 4 points x 4 AOs, then n and grad n partials
+            W n4[4] = {0, 0, 0, 0}, g4[3][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}};
 #pragma unroll
-                for (int r = 0; r < 96 / G; ++r) t[r] = (W)0;
-                const W *ph = s.phi + gp * NP;
-                for (int k = 0; k < N; ++k) {
-                    const W a = ph[k];
-                    const W *rr = s.rho + k * NP + gl;
+            for (int j = 0; j < QJ; ++j) {
+                const int q = lg + j * LG;
+                if (q < NQ) {
+                    W t[4][4];
 #pragma unroll
-                    for (int r = 0; r < 96 / G; ++r)
-                        if (r * G < NP) t[r] += a * rr[r * G];
-                }
+                    for (int a = 0; a < 4; ++a)
 #pragma unroll
-                for (int r = 0; r < 96 / G; ++r)
-                    if (r * G < NP) s.tw[gp * NP + gl + r * G] = t[r];
-            }
-            __syncthreads();
-            {   // n = t . phi, grad n = 2 t . grad phi  (G lanes per point, shuffle tree)
-                W n = 0, gx = 0, gy = 0, gz = 0;
-                for (int mu = gl; mu < N; mu += G) {
-                    const W tv = s.tw[gp * NP + mu];
-                    n += tv * s.phi[gp * NP + mu];
-                    gx += tv * s.phi[plane + gp * NP + mu];
-                    gy += tv * s.phi[2 * plane + gp * NP + mu];
-                    gz += tv * s.phi[3 * plane + gp * NP + mu];
-                }
+                        for (int c = 0; c < 4; ++c) t[a][c] = (W)0;
+                    for (int k = 0; k < N; ++k) {
+                        W f[4], r4[4];
+                        Vec4<W>::ld(phi + swz<BP>(k, 4 * pg), f);
+                        Vec4<W>::ld(rho + k * NP + 4 * q, r4);
 #pragma unroll
-                for (int o = 1; o < G; o <<= 1) {
-                    n += __shfl_xor_sync(0xffffffffu, n, o);
-                    gx += __shfl_xor_sync(0xffffffffu, gx, o);
-                    gy += __shfl_xor_sync(0xffffffffu, gy, o);
-                    gz += __shfl_xor_sync(0xffffffffu, gz, o);
-                }
-                if (gl == 0 && gp < nb) {
-                    double *d = s.dn + 4 * (sub + gp);
-                    d[0] = (double)n;
-                    d[1] = (double)(W)(2 * gx);
-                    d[2] = (double)(W)(2 * gy);
-                    d[3] = (double)(W)(2 * gz);
+                        for (int a = 0; a < 4; ++a)
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) t[a][c] += f[a] * r4[c];
+                    }
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const int nu = 4 * q + c;
+                        W f0[4], f1[4], f2[4], f3[4];
+                        Vec4<W>::ld(phi + swz<BP>(nu, 4 * pg), f0);
+                        Vec4<W>::ld(phi + PL + swz<BP>(nu, 4 * pg), f1);
+                        Vec4<W>::ld(phi + 2 * PL + swz<BP>(nu, 4 * pg), f2);
+                        Vec4<W>::ld(phi + 3 * PL + swz<BP>(nu, 4 * pg), f3);
+#pragma unroll
+                        for (int a = 0; a < 4; ++a) {
+                            n4[a] += t[a][c] * f0[a];
+                            g4[0][a] += t[a][c] * f1[a];
+                            g4[1][a] += t[a][c] * f2[a];
+                            g4[2][a] += t[a][c] * f3[a];
+                        }
+                    }
                 }
             }
-            __syncthreads();
-        }
-        // ---- pass B: functional, one thread per point
-        if (tid < nsb) {
-            double *d = s.dn + 4 * tid;
-            const double n = d[0], gx = d[1], gy = d[2], gz = d[3];
-            const double sig = (double)(W)((W)gx * (W)gx + (W)gy * (W)gy + (W)gz * (W)gz);
-            const XCOut o = b3lyp_point(n, sig);
-            if (!(isfinite(o.exc) && isfinite(o.vrho) && isfinite(o.vsigma))) bad = 1;
-            const double w = s.pt[4 * tid + 3];
-            e_acc += w * n * (double)(W)o.exc;
-            const double ww = (double)(W)w;
-            const double a = (double)(W)(0.5 * ww * (double)(W)o.vrho);
-            const double bb = (double)(W)(2.0 * ww * (double)(W)o.vsigma);
-            d[0] = a;
-            d[1] = bb * gx;
-            d[2] = bb * gy;
-            d[3] = bb * gz;
+#pragma unroll
+            for (int o = 1; o < LG; o <<= 1)
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    n4[a] += __shfl_xor_sync(0xffffffffu, n4[a], o);
+                    g4[0][a] += __shfl_xor_sync(0xffffffffu, g4[0][a], o);
+                    g4[1][a] += __shfl_xor_sync(0xffffffffu, g4[1][a], o);
+                    g4[2][a] += __shfl_xor_sync(0xffffffffu, g4[2][a], o);
+                }
+            if (lg == 0)
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    double *d = dn + 4 * (4 * pg + a);
+                    d[0] = (double)n4[a];
+                    d[1] = (double)(W)(2 * g4[0][a]);
+                    d[2] = (double)(W)(2 * g4[1][a]);
+                    d[3] = (double)(W)(2 * g4[2][a]);
+                }
         }
         __syncthreads();
-        // ---- pass C: V += phi^T (a phi + b . grad phi)
-        for (int sub = 0; sub < nsb; sub += BP) {
-            const int nb = min(BP, nsb - sub);
-            xc_eval_phi(s, nsh, NP, BP, sub, nb);
-            __syncthreads();
-            for (int t = tid; t < BP * NP; t += XC_THREADS) {
-                const int p = t / NP;
-                const double *d = s.dn + 4 * (sub + p);
-                W v = (W)0;
-                if (p < nb)
-                    v = (W)d[0] * s.phi[t] + (W)d[1] * s.phi[plane + t] + (W)d[2] * s.phi[2 * plane + t] +
-                        (W)d[3] * s.phi[3 * plane + t];
-                s.tw[t] = v;
+        if (tid < BP) {   // ---- functional (f64), one thread per point
+            double *d = dn + 4 * tid;
+            if (tid < nb) {
+                const double n = d[0], gx = d[1], gy = d[2], gz = d[3];
+                const double sig = (double)((W)gx * (W)gx + (W)gy * (W)gy + (W)gz * (W)gz);
+                const XCOut o = b3lyp_point(n, sig);
+                if (!(isfinite(o.exc) && isfinite(o.vrho) && isfinite(o.vsigma))) bad = 1;
+                const double w = pt[4 * tid + 3];
+                e_acc += w * n * (double)(W)o.exc;
+                const double ww = (double)(W)w;
+                const double a = (double)(W)(0.5 * ww * (double)(W)o.vrho);
+                const double bb = (double)(W)(2.0 * ww * (double)(W)o.vsigma);
+                d[0] = a;
+                d[1] = bb * gx;
+                d[2] = bb * gy;
+                d[3] = bb * gz;
+            } else {
+                d[0] = d[1] = d[2] = d[3] = 0.0;
             }
-            __syncthreads();
-            for (int p = 0; p < nb; ++p) {
-                const W *ph = s.phi + p * NP + ty;
-                const W *wv = s.tw + p * NP + tx;
-                W fa[6], fb[6];
+        }
+        __syncthreads();
+        for (int t = tid; t < PL; t += XC_THREADS) {       // ---- wv = a phi + b . grad phi
+            const int row = t / BP, p = t % BP;
+            const double *d = dn + 4 * p;
+            const int o = swz<BP>(row, p);
+            wv[o] = (W)d[0] * phi[o] + (W)d[1] * phi[PL + o] + (W)d[2] * phi[2 * PL + o] + (W)d[3] * phi[3 * PL + o];
+        }
+        __syncthreads();
 #pragma unroll
-                for (int a = 0; a < 6; ++a) {
-                    fa[a] = a < nblk16 ? ph[16 * a] : (W)0;
-                    fb[a] = a < nblk16 ? wv[16 * a] : (W)0;
+        for (int j = 0; j < TJ; ++j) {                     // ---- V += phi wv^T, 4 x 4 tiles
+            const int T = tid + j * XC_THREADS;
+            if (T < NT) {
+                const int qa = T / NQ, qb = T % NQ;
+                for (int p4 = 0; p4 < BP; p4 += 4) {
+                    W fa[4][4], fb[4][4];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) {
+                        Vec4<W>::ld(phi + swz<BP>(4 * qa + a, p4), fa[a]);
+                        Vec4<W>::ld(wv + swz<BP>(4 * qb + a, p4), fb[a]);
+                    }
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+#pragma unroll
+                            for (int pp = 0; pp < 4; ++pp) acc[j][a][c] += fa[a][pp] * fb[c][pp];
                 }
-#pragma unroll
-                for (int a = 0; a < 6; ++a)
-#pragma unroll
-                    for (int c = 0; c < 6; ++c) acc[a][c] += fa[a] * fb[c];
             }
-            __syncthreads();
         }
     }
-    double *Vp = b.Vpart + b.m_V0[m] + (int64_t)(cta - b.m_xccta0[m]) * N * N;
+    const int local = cta - b.m_xccta0[m];
+    double *Vp = b.Vpart + b.m_V0[m] + (int64_t)local * N * N;
 #pragma unroll
-    for (int a = 0; a < 6; ++a)
+    for (int j = 0; j < TJ; ++j) {
+        const int T = tid + j * XC_THREADS;
+        if (T < NT) {
+            const int qa = T / NQ, qb = T % NQ;
 #pragma unroll
-        for (int c = 0; c < 6; ++c) {
-            const int mu = ty + 16 * a, nu = tx + 16 * c;
-            if (mu < N && nu < N) Vp[mu * N + nu] = (double)acc[a][c];
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int mu = 4 * qa + a, nu = 4 * qb + c;
+                    if (mu < N && nu < N) Vp[mu * N + nu] = (double)acc[j][a][c];
+                }
         }
-    const double e = block_sum(e_acc, s.red);
+    }
+    const double e = block_sum(e_acc, red);
     if (tid == 0) b.Epart[cta] = e;
     if (bad) atomicOr(b.status + m, DFTB_ST_XC_NONFINITE);
 }
 
-template <typename W>
-static size_t xc_smem(int NP, int BP, int nsh_max) {
-    size_t w = (size_t)NP * NP + 5 * (size_t)BP * NP + 2;
-    return sizeof(W) * w + 16 + sizeof(double) * (8 * XC_SB + XC_SHD * (size_t)nsh_max + 32);
+template <typename W, int NQ, int BP>
+static void launch_bucket(const DevBatch &b, const int *ctas, int n, int nsh_max, cudaStream_t s) {
+    const size_t sm = XCL<W, NQ, BP>::bytes(nsh_max);
+    cudaFuncSetAttribute(k_xc<W, NQ, BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_xc<W, NQ, BP><<<n, XC_THREADS, sm, s>>>(b, ctas);
 }
 
-template <typename W>
-static void launch_xc_t(const DevBatch &b, int nmax, int nsh_max, cudaStream_t s) {
-    const int NP = (nmax + 15) & ~15;
-    size_t sm = xc_smem<W>(NP, 32, nsh_max);
-    if (sm <= 227 * 1024) {
-        cudaFuncSetAttribute(k_xc<W, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_xc<W, 32><<<b.n_xc_cta, XC_THREADS, sm, s>>>(b);
-    } else {
-        sm = xc_smem<W>(NP, 16, nsh_max);
-        cudaFuncSetAttribute(k_xc<W, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_xc<W, 16><<<b.n_xc_cta, XC_THREADS, sm, s>>>(b);
-    }
+template <typename W, int BP, int BPL>
+static void launch_xc_t(const DevBatch &b, const int *bucket_ctas, const int *bucket_n, int nsh_max,
+                        cudaStream_t s) {
+    // BP points per sub-block for N <= 64, BPL for larger N (keeps 2 CTAs/SM in f32)
+    // buckets: NQ = 4, 8, 12, 16, 20, 24 (N <= 16, 32, ..., 96)
+    const int *c = bucket_ctas;
+    if (bucket_n[0]) launch_bucket<W, 4, BP>(b, c, bucket_n[0], nsh_max, s);
+    c += bucket_n[0];
+    if (bucket_n[1]) launch_bucket<W, 8, BP>(b, c, bucket_n[1], nsh_max, s);
+    c += bucket_n[1];
+    if (bucket_n[2]) launch_bucket<W, 12, BP>(b, c, bucket_n[2], nsh_max, s);
+    c += bucket_n[2];
+    if (bucket_n[3]) launch_bucket<W, 16, BP>(b, c, bucket_n[3], nsh_max, s);
+    c += bucket_n[3];
+    if (bucket_n[4]) launch_bucket<W, 20, BPL>(b, c, bucket_n[4], nsh_max, s);
+    c += bucket_n[4];
+    if (bucket_n[5]) launch_bucket<W, 24, BPL>(b, c, bucket_n[5], nsh_max, s);
 }
 
-void launch_xc(const DevBatch &b, int nmax, int nsh_max, cudaStream_t s) {
-    if (b.n_xc_cta == 0) return;
-    if (b.prec == 0) launch_xc_t<double>(b, nmax, nsh_max, s);
-    else launch_xc_t<float>(b, nmax, nsh_max, s);
+// bucket_ctas: device array of CTA indices grouped by bucket; bucket_n: host counts [6]
+int launch_xc(const DevBatch &b, const int *bucket_ctas, const int *bucket_n, int nsh_max, cudaStream_t s) {
+    if (b.n_xc_cta == 0) return 0;
+    if (b.prec == 0) launch_xc_t<double, 32, 32>(b, bucket_ctas, bucket_n, nsh_max, s);
+    else launch_xc_t<float, 64, 32>(b, bucket_ctas, bucket_n, nsh_max, s);
+    int k = 0;
+    for (int i = 0; i < 6; ++i) k += bucket_n[i] > 0;
+    return k;
 }
 
 }  // namespace dftb
