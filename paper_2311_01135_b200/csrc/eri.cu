@@ -147,12 +147,19 @@ __global__ void __launch_bounds__(128) k_eri(DevBatch b, int cls, double eps, do
 #pragma unroll
             for (int y = 0; y < NKS; ++y) out[x][y] = 0.0;
         eri_quartet<KA, KB, KC, KD, KC0, NKS>(V, Pp, Qp, A, B, C, D, b.boys, prim_cut, out);
+        // single writer per canonical element: for a diagonal shell pair only the
+        // (i >= j) component writes, for a diagonal quartet only the (ij >= kl) image
+        const bool dab = b.p_sa[Pp] == b.p_sb[Pp], dcd = b.p_sa[Qp] == b.p_sb[Qp], dpq = Pp == Qp;
 #pragma unroll
         for (int x = 0; x < NA * NB; ++x)
 #pragma unroll
             for (int y = 0; y < NKS; ++y) {
                 const int kc = KC0 + y;
-                store_eri(eri, base, ia + x / NB, ib + x % NB, ic + kc / ND, id + kc % ND, out[x][y]);
+                const int i = ia + x / NB, j = ib + x % NB, k = ic + kc / ND, l = id + kc % ND;
+                if (dab && i < j) continue;
+                if (dcd && k < l) continue;
+                if (dpq && pidx(i, j) < pidx(k, l)) continue;
+                store_eri(eri, base, i, j, k, l, out[x][y]);
             }
     });
 }
@@ -183,10 +190,12 @@ __global__ void __launch_bounds__(128) k_schwarz(DevBatch b, int which) {
 #pragma unroll
             for (int y = 0; y < NKS; ++y) out[x][y] = 0.0;
         eri_quartet<KA, KB, KA, KB, KC0, NKS>(V, Pp, Pp, A, B, A, B, b.boys, 0.0, out);
+        const bool dab = b.p_sa[Pp] == b.p_sb[Pp];
 #pragma unroll
         for (int y = 0; y < NKS; ++y) {
             const int c = KC0 + y;
             const double v = out[c][y];
+            if (dab && c / NB < c % NB) continue;   // single writer for symmetric components
             qao[pidx(ia + c / NB, ib + c % NB)] = sqrt(fmax(v, 0.0));
         }
     });

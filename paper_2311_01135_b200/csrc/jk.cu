@@ -7,17 +7,18 @@
 // for one or two values of i.  Row P holds (ij|kl) for all Q = (k, l) <= P.  For a
 // stored element the 8 images contribute J_P += v rho~_Q, J_Q += v rho~_P and —
 // recording each K contribution at (a,d) or its transpose — only G[i][.] and G[j][.]
-// updates (K = -(G + G^T)/4 at the end).  Per row the CTA expands the row into a
-// symmetric N x N shared tile T and computes two GEMVs (T rho_j, T rho_i) and one
-// dot product.  G_i accumulates in registers across the CTA's rows, the J_Q
-// scatter accumulates in registers (thread t owns Q = t mod 256), G_j rows and J
-// partials are written once and summed in a fixed order by the SCF post kernel.
+// updates (K = -(G + G^T)/4 at the end).  Per row the CTA computes two GEMVs with
+// the row's symmetric ket matrix T (T rho_j, T rho_i), read straight from the
+// staged packed row, and one dot product.  G_i accumulates in registers across the
+// CTA's rows, the J_Q scatter accumulates in registers (thread t owns Q = t mod
+// 256), G_j rows and J partials are written once and summed in a fixed order by the
+// SCF post kernel.  One CTA barrier per row.
 //
 // Data movement: rows are 16-byte padded in HBM and prefetched whole with
 // cp.async.bulk (TMA bulk copy, mbarrier completion) into a double-buffered
 // staging area while the previous row is being digested; the store is streamed
-// exactly once per SCF iteration.  In the f32 build the rho / T tiles are kept in
-// f32 shared memory (rho is f32-valued there), products are formed in f64.
+// exactly once per SCF iteration.  In the f32 build rho is kept in f32 shared
+// memory (it is f32-valued there); products are always formed in f64.
 #include "common.cuh"
 
 namespace dftb {
@@ -51,11 +52,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 }
 
 struct JKLayout {
-    size_t stage, rho, T, lut, wpart, total;
+    size_t stage, rho, lut, wpart, total;
 };
 
-template <typename ST, typename RT>
+constexpr int JK_MAXROWS = NMAX + 1;   // rows per CTA: (i0 + 1) + (i1 + 1) = N + 1
+
+template <typename ST, typename RT_unused>
 HD JKLayout jk_layout(int N, int nbuf) {
+    using RT = double;
     const int g = 16 / (int)sizeof(ST);
     const size_t npp = (size_t)N * (N + 1) / 2;
     JKLayout L;
@@ -63,15 +67,19 @@ HD JKLayout jk_layout(int N, int nbuf) {
     L.stage = o; o += (size_t)nbuf * rowpad((int64_t)npp, g) * sizeof(ST);
     o = (o + 15) & ~(size_t)15;
     L.rho = o; o += (size_t)N * N * sizeof(RT);
-    L.T = o; o += (size_t)N * N * sizeof(RT);
     o = (o + 15) & ~(size_t)15;
     L.lut = o; o += npp * sizeof(uint16_t);
     o = (o + 15) & ~(size_t)15;
-    L.wpart = o; o += 8 * sizeof(double);
+    L.wpart = o; o += (size_t)JK_MAXROWS * (JK_THREADS / 32) * sizeof(double);
     L.total = o;
     return L;
 }
 
+// Row P = (i, j) of the packed store, staged in shared memory, is digested without
+// expanding it: element (k, l) of the row sits at tri(k) + l, so the column t of the
+// symmetric ket matrix T is {row[tri(n) + t] : n >= t} U {row[tri(t) + n] : n < t}.
+// Across a warp, tri(t) + n hits 32 distinct banks (triangular numbers are a
+// permutation mod 32), so both walks are conflict-free.
 template <typename ST, typename RT>
 __global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, int nbuf) {
     extern __shared__ __align__(128) unsigned char sm[];
@@ -85,8 +93,7 @@ __global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, int nbuf) {
     uint64_t *bar = (uint64_t *)sm;
     ST *stage = (ST *)(sm + L.stage);
     const int64_t stride = rowpad(npp, g);
-    RT *rho = (RT *)(sm + L.rho);
-    RT *Tm = (RT *)(sm + L.T);
+    double *rho = (double *)(sm + L.rho);
     uint16_t *lut = (uint16_t *)(sm + L.lut);
     double *wpart = (double *)(sm + L.wpart);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -111,7 +118,7 @@ __global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, int nbuf) {
     if (tid == 0)
         for (int r = 0; r < nbuf && r < nrows; ++r) issue(r);
     const double *rg = b.rho + b.m_mat0[m];
-    for (int t = tid; t < N * N; t += JK_THREADS) rho[t] = (RT)rg[t];
+    for (int t = tid; t < N * N; t += JK_THREADS) rho[t] = rg[t];
     for (int k = tid; k < N; k += JK_THREADS)
         for (int l = 0; l <= k; ++l) lut[tri(k) + l] = (uint16_t)((k << 8) | l);
     __syncthreads();
@@ -127,8 +134,8 @@ __global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, int nbuf) {
         const int64_t P = tri(i) + j;
         const ST *row = stage + (r % nbuf) * stride;
         mbar_wait(bar + (r % nbuf), (uint32_t)((r / nbuf) & 1));
-        // ---- phase 1: expand the row into T, J_own dot product, scattered J_Q
-        const double rt = (double)rho[i * N + j] * (i != j ? 2.0 : 1.0);
+        // ---- J: own dot product and the scattered J_Q (thread owns Q = tid mod 256)
+        const double rt = rho[i * N + j] * (i != j ? 2.0 : 1.0);
         double jown = 0.0;
 #pragma unroll
         for (int q = 0; q < JK_NREG; ++q) {
@@ -136,44 +143,72 @@ __global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, int nbuf) {
             if (e <= P) {
                 const double v = (double)row[e];
                 const int kl = lut[e], k = kl >> 8, l = kl & 255;
-                const RT c = (RT)(e == P ? v : 2.0 * v);
-                Tm[k * N + l] = c;
-                Tm[l * N + k] = c;
-                jown += v * (double)rho[k * N + l] * (k != l ? 2.0 : 1.0);
+                jown += v * rho[k * N + l] * (k != l ? 2.0 : 1.0);
                 if (e < P) jsc[q] += v * rt;
             }
         }
-        for (int l = j + 1 + tid; l <= i; l += JK_THREADS) {
-            Tm[i * N + l] = (RT)0;
-            Tm[l * N + i] = (RT)0;
+        // ---- K: G_i[t] += (T rho_j)[t] and G_j[t] = (T rho_i)[t], T read from the packed row.
+        // One thread forms both dot products for output t over n = sl, sl+S, ... (S lanes per
+        // output, combined by a shuffle tree).  T[n][t] = 2 v(e) except the row's own
+        // element e = P (weight 1), corrected once; no per-element bounds checks.
+        {
+            const int ni = i + 1;
+            const int S = ni * 8 <= JK_THREADS ? 8 : ni * 4 <= JK_THREADS ? 4 : ni * 2 <= JK_THREADS ? 2 : 1;
+            const int t = tid / S, sl = tid % S;
+            double ai = 0.0, aj = 0.0;
+            if (t < ni) {
+                const double *rj = rho + j * N, *ri = rho + i * N;
+                const int tt = (int)tri(t);
+                // walk 1: (t, n), n < n1 ; valid while tt + n <= P
+                const int n1 = t < i ? t : min(t, j + 1);
+                for (int n = sl; n < n1; n += S) {
+                    const double v = (double)row[tt + n];
+                    ai += v * rj[n];
+                    aj += v * ri[n];
+                }
+                // walk 2: (n, t), t <= n <= n2 ; row index tri(n) + t
+                const int n2 = t <= j ? i : i - 1;
+                int n = t + sl;
+                int e = (int)tri(n) + t;
+                for (; n <= n2; n += S) {
+                    const double v = (double)row[e];
+                    ai += v * rj[n];
+                    aj += v * ri[n];
+                    // tri(n + S) - tri(n) = S n + S (S + 1) / 2
+                    e += S * n + (S * (S + 1) >> 1);
+                }
+                ai *= 2.0;
+                aj *= 2.0;
+                if (sl == 0) {
+                    const double vp = (double)row[P];
+                    if (t == j) { ai -= vp * rj[i]; aj -= vp * ri[i]; }
+                    else if (t == i) { ai -= vp * rj[j]; aj -= vp * ri[j]; }
+                }
+            }
+            for (int o = S >> 1; o > 0; o >>= 1) {
+                ai += __shfl_xor_sync(0xffffffffu, ai, o);
+                aj += __shfl_xor_sync(0xffffffffu, aj, o);
+            }
+            if (sl == 0 && t < ni) {
+                gi += ai;
+                if (j < i) Gp[P * N + t] = aj;
+                if (j == i) {
+                    Gp[(tri(i) + i) * N + t] = gi;
+                    gi = 0.0;
+                }
+            }
         }
         jown = warp_sum(jown);
-        if (lane == 0) wpart[warp] = jown;
-        __syncthreads();
-        if (tid == 0) {
-            double s = 0.0;
-            for (int w = 0; w < JK_THREADS / 32; ++w) s += wpart[w];
-            Jp[P] = s;
-            if (r + nbuf < nrows) issue(r + nbuf);   // this row's staging buffer is free again
-        }
-        // ---- phase 2: G_i[t] += (T rho_j)[t] (threads 0..i), G_j[t] = (T rho_i)[t] (threads 128..)
-        if (tid <= i) {
-            double a = 0.0;
-            const RT *rj = rho + j * N;
-            for (int n = 0; n <= i; ++n) a += (double)Tm[n * N + tid] * (double)rj[n];
-            gi += a;
-        } else if (tid >= 128 && tid - 128 <= i && j < i) {
-            const int t = tid - 128;
-            double c2 = 0.0;
-            const RT *ri = rho + i * N;
-            for (int n = 0; n <= i; ++n) c2 += (double)Tm[n * N + t] * (double)ri[n];
-            Gp[P * N + t] = c2;
-        }
-        if (j == i) {
-            if (tid <= i) Gp[(tri(i) + i) * N + tid] = gi;
-            gi = 0.0;
-        }
-        __syncthreads();
+        if (lane == 0) wpart[r * (JK_THREADS / 32) + warp] = jown;
+        __syncthreads();                              // row r fully consumed: refill its buffer
+        if (tid == 0 && r + nbuf < nrows) issue(r + nbuf);
+    }
+    for (int r = tid; r < nrows; r += JK_THREADS) {
+        int i, j;
+        row_ij(r, i, j);
+        double s = 0.0;
+        for (int w = 0; w < JK_THREADS / 32; ++w) s += wpart[r * (JK_THREADS / 32) + w];
+        Jp[tri(i) + j] = s;
     }
     const int local = cta - b.m_jkcta0[m];
     double *Js = Jp + (int64_t)(1 + local) * npp;

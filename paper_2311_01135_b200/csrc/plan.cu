@@ -374,6 +374,11 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
     d.max_it = maxit;
     d.dbg = PTR(long long, o_dbg);
 #undef PTR
+    ce = cudaMemsetAsync(p->mem + p->work_off, 0, p->mem_bytes - p->work_off, st);
+    if (ce != cudaSuccess) {
+        dftb_plan_destroy(p);
+        return fail(DFTB_ECUDA, std::string("memset: ") + cudaGetErrorString(ce));
+    }
     const double *boys = nullptr;
     int rc = ensure_boys(p->device, &boys);
     if (rc) { dftb_plan_destroy(p); return rc; }
@@ -526,10 +531,11 @@ int dftb_plan_launch_count(const dftb_plan *p, int64_t *count) {
 
 int dftb_plan_info(const dftb_plan *p, int64_t *info, int n) {
     if (!p) return fail(DFTB_EINVAL, "null plan");
-    int64_t v[16] = {p->d.n_mol, p->d.n_pair, p->d.n_pts, (int64_t)p->mem_bytes, (int64_t)p->eri_bytes,
+    int64_t v[20] = {p->d.n_mol, p->d.n_pair, p->d.n_pts, (int64_t)p->mem_bytes, (int64_t)p->eri_bytes,
                      p->cls_tot[0], p->cls_tot[1], p->cls_tot[2], p->cls_tot[3], p->cls_tot[4], p->cls_tot[5],
-                     p->d.n_jk_cta, p->d.n_xc_cta, p->nmax, p->mat0[p->d.n_mol], p->launches};
-    for (int k = 0; k < n && k < 16; ++k) info[k] = v[k];
+                     p->d.n_jk_cta, p->d.n_xc_cta, p->nmax, p->mat0[p->d.n_mol], p->launches,
+                     (int64_t)p->in_bytes, p->pair_tot[0], p->pair_tot[1], p->pair_tot[2]};
+    for (int k = 0; k < n && k < 20; ++k) info[k] = v[k];
     return 0;
 }
 

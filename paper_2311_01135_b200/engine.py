@@ -130,10 +130,11 @@ class Plan:
         return int(c.value)
 
     def info(self) -> dict:
-        v = np.zeros(16, np.int64)
-        _lib.check(self.lib.dftb_plan_info(self.h, v.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), 16))
+        v = np.zeros(20, np.int64)
+        _lib.check(self.lib.dftb_plan_info(self.h, v.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), 20))
         keys = ["n_mol", "n_pair", "n_pts", "mem_bytes", "eri_bytes", "q_llll", "q_llls", "q_llss",
-                "q_lsls", "q_lsss", "q_ssss", "n_jk_cta", "n_xc_cta", "nmax", "mat_elems", "launches"]
+                "q_lsls", "q_lsss", "q_ssss", "n_jk_cta", "n_xc_cta", "nmax", "mat_elems", "launches",
+                "h2d_bytes", "pairs_ll", "pairs_ls", "pairs_ss"]
         return dict(zip(keys, (int(x) for x in v)))
 
     def get(self, which: str, mol: int = 0) -> np.ndarray:
