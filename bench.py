@@ -165,23 +165,34 @@ def _oracle_worker(args):
     return r.E_total
 
 
-def cpu_sample(n_mol: int, seed: int, cores: int):
-    """Time the oracle restatement of the reference (one process per core, 1 thread each,
-    like deskdft.pipeline.run) on n_mol molecules of the workload.  Returns mol/s."""
-    import multiprocessing as mp
+class CpuArm:
+    """The oracle restatement of the reference (one process per core, 1 thread each, like
+    deskdft.pipeline.run) timed on samples of the workload."""
 
-    from paper_2311_01135_b200 import synth
+    def __init__(self, cores: int):
+        import multiprocessing as mp
 
-    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
-    mols = synth.batch(n_mol, HEAVY, seed=seed)
-    jobs = [(m.atomic_numbers, m.positions.tolist()) for m in mols]
-    ctx = mp.get_context("spawn")
-    with ctx.Pool(cores) as pool:
-        pool.map(_oracle_worker, jobs[:cores])          # warm (imports, scipy tables)
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
+        self.cores = cores
+        self.pool = mp.get_context("spawn").Pool(cores)
+        self.pool.map(_oracle_worker, self._jobs(cores, 4999))      # warm: imports, scipy tables
+
+    @staticmethod
+    def _jobs(n_mol, seed):
+        from paper_2311_01135_b200 import synth
+
+        return [(m.atomic_numbers, m.positions.tolist()) for m in synth.batch(n_mol, HEAVY, seed=seed)]
+
+    def sample(self, n_mol: int, seed: int):
+        jobs = self._jobs(n_mol, seed)
         t = time.perf_counter()
-        pool.map(_oracle_worker, jobs)
+        self.pool.map(_oracle_worker, jobs)
         dt = time.perf_counter() - t
-    return n_mol / dt, dt
+        return n_mol / dt, dt
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
 
 
 def run_reference(args, ws, rank):
@@ -189,11 +200,13 @@ def run_reference(args, ws, rank):
         return
     cores = os.cpu_count() or 1
     per_step = cores  # one molecule per core per step: ~5-15 s of CPU work
+    arm = CpuArm(cores)
     vals = []
     for k in range(args.warmup + args.steps):
-        v, dt = cpu_sample(per_step, seed=5000 + k, cores=cores)
+        v, dt = arm.sample(per_step, seed=5000 + k)
         if k >= args.warmup:
             vals.append(v)
+    arm.close()
     value = float(np.mean(vals))
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000.0 * per_step / value, "higher_is_better": True,
@@ -316,7 +329,9 @@ def run_ours(args, ws, rank, local):
     }
     if args.cpu_baseline and rank == 0 and ws == 1:
         cores = os.cpu_count() or 1
-        v, dt = cpu_sample(cores, seed=7000, cores=cores)
+        arm = CpuArm(cores)
+        v, dt = arm.sample(cores, seed=7000)
+        arm.close()
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                                 "sample": f"{cores} molecules (1 per core) of the configs[1] generator, "
                                           f"{dt:.1f} s wall; oracle/ restatement, one process per core"}
