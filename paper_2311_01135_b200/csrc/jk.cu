@@ -51,36 +51,40 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
+constexpr int JK_R = 4;                  // rows per chunk (one TMA bulk copy)
+constexpr int JK_G = JK_THREADS / JK_R;  // threads per row (64)
+
 struct JKLayout {
-    size_t stage, rho, lut, wpart, total;
+    size_t stage, rho, lut, gpart, total;
+    int64_t chunk;                        // elements per staging buffer
 };
 
-constexpr int JK_MAXROWS = NMAX + 1;   // rows per CTA: (i0 + 1) + (i1 + 1) = N + 1
-
-template <typename ST, typename RT_unused>
+template <typename ST>
 HD JKLayout jk_layout(int N, int nbuf) {
-    using RT = double;
     const int g = 16 / (int)sizeof(ST);
-    const size_t npp = (size_t)N * (N + 1) / 2;
+    const int64_t npp = (int64_t)N * (N + 1) / 2;
     JKLayout L;
+    L.chunk = (int64_t)JK_R * rowpad(npp, g);
     size_t o = 64;                                    // mbarriers
-    L.stage = o; o += (size_t)nbuf * rowpad((int64_t)npp, g) * sizeof(ST);
+    L.stage = o; o += (size_t)nbuf * L.chunk * sizeof(ST);
     o = (o + 15) & ~(size_t)15;
-    L.rho = o; o += (size_t)N * N * sizeof(RT);
+    L.rho = o; o += (size_t)N * N * sizeof(double);
+    L.lut = o; o += (size_t)npp * sizeof(uint16_t);
     o = (o + 15) & ~(size_t)15;
-    L.lut = o; o += npp * sizeof(uint16_t);
-    o = (o + 15) & ~(size_t)15;
-    L.wpart = o; o += (size_t)JK_MAXROWS * (JK_THREADS / 32) * sizeof(double);
+    L.gpart = o; o += (size_t)JK_R * 2 * JK_G * sizeof(double);
     L.total = o;
     return L;
 }
 
-// Row P = (i, j) of the packed store, staged in shared memory, is digested without
-// expanding it: element (k, l) of the row sits at tri(k) + l, so the column t of the
-// symmetric ket matrix T is {row[tri(n) + t] : n >= t} U {row[tri(t) + n] : n < t}.
-// Across a warp, tri(t) + n hits 32 distinct banks (triangular numbers are a
-// permutation mod 32), so both walks are conflict-free.
-template <typename ST, typename RT>
+// A CTA digests the rows P = (i, j) of one or two i-slabs in chunks of JK_R consecutive
+// rows (contiguous in HBM -> one cp.async.bulk per chunk, double buffered).  Within a
+// chunk, 64 threads per row form the J_P dot product and the two K GEMVs with the
+// row's symmetric ket matrix T, read straight from the staged packed row:
+//   element (k, l) sits at tri(k) + l, so column t of T is row[tri(t) + n] (n < t) and
+//   row[tri(n) + t] (n >= t); a single merged walk over n keeps every lane busy.
+// The scattered J_Q contributions are done column-wise per chunk by the thread that owns
+// Q (Q = tid mod 256), so they accumulate in registers across the CTA's rows.
+template <typename ST>
 __global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, int nbuf) {
     extern __shared__ __align__(128) unsigned char sm[];
     const int cta = blockIdx.x;
@@ -89,26 +93,31 @@ __global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, int nbuf) {
     const int N = b.m_nao[m];
     const int g = 16 / (int)sizeof(ST);
     const int64_t npp = tri(N);
-    const JKLayout L = jk_layout<ST, RT>(N, nbuf);
+    const JKLayout L = jk_layout<ST>(N, nbuf);
     uint64_t *bar = (uint64_t *)sm;
     ST *stage = (ST *)(sm + L.stage);
-    const int64_t stride = rowpad(npp, g);
     double *rho = (double *)(sm + L.rho);
     uint16_t *lut = (uint16_t *)(sm + L.lut);
-    double *wpart = (double *)(sm + L.wpart);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double *gpart = (double *)(sm + L.gpart);
+    const int tid = threadIdx.x;
+    const int grp = tid / JK_G, gt = tid % JK_G;      // row slot in the chunk, thread in the row
     const ST *eri = (const ST *)b.eri + b.m_eri0[m];
-    const int i0 = b.jk_i0[cta], i1 = b.jk_i1[cta];
-    const int nrow0 = i0 + 1, nrows = nrow0 + (i1 >= 0 ? i1 + 1 : 0);
-    auto row_ij = [&](int r, int &i, int &j) {
-        if (r < nrow0) { i = i0; j = r; } else { i = i1; j = r - nrow0; }
+    const int iv[2] = {b.jk_i0[cta], b.jk_i1[cta]};
+    // chunk list: (slab s, first j); nch0 chunks for the first slab
+    const int nch0 = (iv[0] + JK_R) / JK_R;
+    const int nch = nch0 + (iv[1] >= 0 ? (iv[1] + JK_R) / JK_R : 0);
+    auto chunk_of = [&](int c, int &i, int &j0, int &nr) {
+        const int s = c < nch0 ? 0 : 1, cc = c < nch0 ? c : c - nch0;
+        i = iv[s];
+        j0 = cc * JK_R;
+        nr = min(JK_R, i + 1 - j0);
     };
-    auto issue = [&](int r) {
-        int i, j;
-        row_ij(r, i, j);
-        const int64_t P = tri(i) + j;
-        bulk_row(stage + (r % nbuf) * stride, eri + rowbase(P, g), (uint32_t)(rowpad(P + 1, g) * sizeof(ST)),
-                 bar + (r % nbuf));
+    auto issue = [&](int c) {
+        int i, j0, nr;
+        chunk_of(c, i, j0, nr);
+        const int64_t P0 = tri(i) + j0;
+        const int64_t e0 = rowbase(P0, g), e1 = rowbase(P0 + nr, g);
+        bulk_row(stage + (c % nbuf) * L.chunk, eri + e0, (uint32_t)((e1 - e0) * sizeof(ST)), bar + (c % nbuf));
     };
     if (tid == 0) {
         for (int k = 0; k < nbuf; ++k) mbar_init(bar + k, 1);
@@ -116,7 +125,7 @@ __global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, int nbuf) {
     }
     __syncthreads();
     if (tid == 0)
-        for (int r = 0; r < nbuf && r < nrows; ++r) issue(r);
+        for (int c = 0; c < nbuf && c < nch; ++c) issue(c);
     const double *rg = b.rho + b.m_mat0[m];
     for (int t = tid; t < N * N; t += JK_THREADS) rho[t] = rg[t];
     for (int k = tid; k < N; k += JK_THREADS)
@@ -127,88 +136,102 @@ __global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, int nbuf) {
     for (int q = 0; q < JK_NREG; ++q) jsc[q] = 0.0;
     double *Gp = b.Gpart + b.m_G0[m];
     double *Jp = b.Jpart + b.m_Jp0[m];
-    double gi = 0.0;
-    for (int r = 0; r < nrows; ++r) {
-        int i, j;
-        row_ij(r, i, j);
-        const int64_t P = tri(i) + j;
-        const ST *row = stage + (r % nbuf) * stride;
-        mbar_wait(bar + (r % nbuf), (uint32_t)((r / nbuf) & 1));
-        // ---- J: own dot product and the scattered J_Q (thread owns Q = tid mod 256)
-        const double rt = rho[i * N + j] * (i != j ? 2.0 : 1.0);
-        double jown = 0.0;
-#pragma unroll
-        for (int q = 0; q < JK_NREG; ++q) {
-            const int64_t e = tid + (int64_t)q * JK_THREADS;
-            if (e <= P) {
-                const double v = (double)row[e];
+    double gi0 = 0.0, gi1 = 0.0;                      // G_i[t] partials, t = gt and gt + 64
+    for (int c = 0; c < nch; ++c) {
+        int i, j0, nr;
+        chunk_of(c, i, j0, nr);
+        const int64_t P0 = tri(i) + j0;
+        const ST *cbuf = stage + (c % nbuf) * L.chunk;
+        mbar_wait(bar + (c % nbuf), (uint32_t)((c / nbuf) & 1));
+        const int64_t rb0 = rowbase(P0, g);
+        if (grp < nr) {
+            const int j = j0 + grp;
+            const int P = (int)(P0 + grp);
+            const ST *row = cbuf + (rowbase(P, g) - rb0);
+            // ---- J_P = sum_Q v_PQ rho~_Q  (64 threads, fixed shuffle tree + smem pair sum)
+            double jown = 0.0;
+            for (int e = gt; e <= P; e += JK_G) {
                 const int kl = lut[e], k = kl >> 8, l = kl & 255;
-                jown += v * rho[k * N + l] * (k != l ? 2.0 : 1.0);
-                if (e < P) jsc[q] += v * rt;
+                jown += (double)row[e] * rho[k * N + l] * (k != l ? 2.0 : 1.0);
             }
-        }
-        // ---- K: G_i[t] += (T rho_j)[t] and G_j[t] = (T rho_i)[t], T read from the packed row.
-        // One thread forms both dot products for output t over n = sl, sl+S, ... (S lanes per
-        // output, combined by a shuffle tree).  T[n][t] = 2 v(e) except the row's own
-        // element e = P (weight 1), corrected once; no per-element bounds checks.
-        {
-            const int ni = i + 1;
-            const int S = ni * 8 <= JK_THREADS ? 8 : ni * 4 <= JK_THREADS ? 4 : ni * 2 <= JK_THREADS ? 2 : 1;
-            const int t = tid / S, sl = tid % S;
-            double ai = 0.0, aj = 0.0;
-            if (t < ni) {
-                const double *rj = rho + j * N, *ri = rho + i * N;
+            jown = warp_sum(jown);
+            // ---- K: G_i[t] += (T rho_j)[t], G_j[t] = (T rho_i)[t]
+            const double *rj = rho + j * N, *ri = rho + i * N;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int t = gt + h * JK_G;
+                if (t > i) break;
                 const int tt = (int)tri(t);
-                // walk 1: (t, n), n < n1 ; valid while tt + n <= P
-                const int n1 = t < i ? t : min(t, j + 1);
-                for (int n = sl; n < n1; n += S) {
-                    const double v = (double)row[tt + n];
-                    ai += v * rj[n];
-                    aj += v * ri[n];
+                double ai = 0.0, aj = 0.0;
+                int trin = 0;                         // tri(n)
+                for (int n = 0; n <= i; ++n) {
+                    const int e = n < t ? tt + n : trin + t;
+                    trin += n + 1;
+                    if (e <= P) {
+                        const double v = (double)row[e];
+                        ai += v * rj[n];
+                        aj += v * ri[n];
+                    }
                 }
-                // walk 2: (n, t), t <= n <= n2 ; row index tri(n) + t
-                const int n2 = t <= j ? i : i - 1;
-                int n = t + sl;
-                int e = (int)tri(n) + t;
-                for (; n <= n2; n += S) {
-                    const double v = (double)row[e];
-                    ai += v * rj[n];
-                    aj += v * ri[n];
-                    // tri(n + S) - tri(n) = S n + S (S + 1) / 2
-                    e += S * n + (S * (S + 1) >> 1);
-                }
+                // T = 2 v except the row's own element (weight 1): corrected once
                 ai *= 2.0;
                 aj *= 2.0;
-                if (sl == 0) {
-                    const double vp = (double)row[P];
-                    if (t == j) { ai -= vp * rj[i]; aj -= vp * ri[i]; }
-                    else if (t == i) { ai -= vp * rj[j]; aj -= vp * ri[j]; }
-                }
+                const double vp = (double)row[P];
+                if (t == j) { ai -= vp * rj[i]; aj -= vp * ri[i]; }
+                else if (t == i) { ai -= vp * rj[j]; aj -= vp * ri[j]; }
+                if (h == 0) gi0 += ai; else gi1 += ai;
+                if (j < i) Gp[(int64_t)P * N + t] = aj;
             }
-            for (int o = S >> 1; o > 0; o >>= 1) {
-                ai += __shfl_xor_sync(0xffffffffu, ai, o);
-                aj += __shfl_xor_sync(0xffffffffu, aj, o);
+            if ((tid & 31) == 0) gpart[2 * JK_G * JK_R - 1 - (tid >> 5)] = jown;   // 2 warps per row
+        }
+        // ---- scattered J_Q += v_PQ rho~_P for Q < P, thread-owned Q across the CTA's rows
+        {
+            int off[JK_R];
+            double rt[JK_R];
+#pragma unroll
+            for (int r = 0; r < JK_R; ++r) {
+                const int j = min(j0 + r, i);
+                off[r] = (int)(rowbase(P0 + r, g) - rb0);
+                rt[r] = r < nr ? rho[i * N + j] * (i != j ? 2.0 : 1.0) : 0.0;
             }
-            if (sl == 0 && t < ni) {
-                gi += ai;
-                if (j < i) Gp[P * N + t] = aj;
-                if (j == i) {
-                    Gp[(tri(i) + i) * N + t] = gi;
-                    gi = 0.0;
+            const int Pend = (int)(P0 + nr - 1);      // Q < P for some row of the chunk
+            const int Pfirst = (int)P0;
+#pragma unroll
+            for (int q = 0; q < JK_NREG; ++q) {
+                const int Q = tid + q * JK_THREADS;
+                if (Q >= Pend) break;
+                double acc = 0.0;
+                if (Q < Pfirst) {                     // below every row of the chunk
+#pragma unroll
+                    for (int r = 0; r < JK_R; ++r)
+                        if (r < nr) acc += (double)cbuf[off[r] + Q] * rt[r];
+                } else {
+#pragma unroll
+                    for (int r = 0; r < JK_R; ++r)
+                        if (r < nr && Q < Pfirst + r) acc += (double)cbuf[off[r] + Q] * rt[r];
                 }
+                jsc[q] += acc;
             }
         }
-        jown = warp_sum(jown);
-        if (lane == 0) wpart[r * (JK_THREADS / 32) + warp] = jown;
-        __syncthreads();                              // row r fully consumed: refill its buffer
-        if (tid == 0 && r + nbuf < nrows) issue(r + nbuf);
-    }
-    for (int r = tid; r < nrows; r += JK_THREADS) {
-        int i, j;
-        row_ij(r, i, j);
-        double s = 0.0;
-        for (int w = 0; w < JK_THREADS / 32; ++w) s += wpart[r * (JK_THREADS / 32) + w];
-        Jp[tri(i) + j] = s;
+        __syncthreads();                              // chunk consumed; J_P partials visible
+        if (tid < nr) {
+            const int w0 = 2 * JK_G * JK_R - 1 - 2 * tid;
+            Jp[P0 + tid] = gpart[w0] + gpart[w0 - 1];
+        }
+        if (tid == 0 && c + nbuf < nch) issue(c + nbuf);
+        if (j0 + nr == i + 1) {                       // slab complete: reduce G_i over the row groups
+            __syncthreads();
+            gpart[grp * 2 * JK_G + gt] = gi0;
+            gpart[grp * 2 * JK_G + JK_G + gt] = gi1;
+            __syncthreads();
+            if (tid <= i) {
+                double s = 0.0;
+                for (int r = 0; r < JK_R; ++r) s += gpart[r * 2 * JK_G + tid];
+                Gp[(tri(i) + i) * N + tid] = s;
+            }
+            gi0 = gi1 = 0.0;
+            __syncthreads();
+        }
     }
     const int local = cta - b.m_jkcta0[m];
     double *Js = Jp + (int64_t)(1 + local) * npp;
@@ -219,21 +242,21 @@ __global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, int nbuf) {
     }
 }
 
-template <typename ST, typename RT>
+template <typename ST>
 static void launch_jk_t(const DevBatch &b, int nmax, cudaStream_t s) {
     int nbuf = 2;
-    size_t sm = jk_layout<ST, RT>(nmax, 2).total;
+    size_t sm = jk_layout<ST>(nmax, 2).total;
     if (sm > 227 * 1024) {
         nbuf = 1;
-        sm = jk_layout<ST, RT>(nmax, 1).total;
+        sm = jk_layout<ST>(nmax, 1).total;
     }
-    cudaFuncSetAttribute(k_jk<ST, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_jk<ST, RT><<<b.n_jk_cta, JK_THREADS, sm, s>>>(b, nbuf);
+    cudaFuncSetAttribute(k_jk<ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_jk<ST><<<b.n_jk_cta, JK_THREADS, sm, s>>>(b, nbuf);
 }
 
 void launch_jk(const DevBatch &b, int nmax, cudaStream_t s) {
-    if (b.prec == 0) launch_jk_t<double, double>(b, nmax, s);
-    else launch_jk_t<float, float>(b, nmax, s);
+    if (b.prec == 0) launch_jk_t<double>(b, nmax, s);
+    else launch_jk_t<float>(b, nmax, s);
 }
 
 }  // namespace dftb

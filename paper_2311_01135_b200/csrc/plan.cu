@@ -70,6 +70,7 @@ struct dftb_plan {
     cudaEvent_t ev[8] = {nullptr};
     double stage_ms[8] = {0};
     int device = 0;
+    cudaStream_t stream = nullptr;
 };
 
 // ------------------------------------------------------------------ Boys table (per device)
@@ -112,7 +113,7 @@ int dftb_device_count(int *count) {
 
 int dftb_plan_destroy(dftb_plan *p) {
     if (!p) return 0;
-    if (p->mem) cudaFree(p->mem);
+    if (p->mem) cudaFreeAsync(p->mem, p->stream);   // back to the retained stream-ordered pool
     for (auto &e : p->ev)
         if (e) cudaEventDestroy(e);
     delete p;
@@ -321,7 +322,19 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
     p->eri_bytes = (size_t)eri0[nm] * esz;
     p->mem_bytes = (L.off + 255) & ~(size_t)255;
     // ---------------- allocate + upload
-    cudaError_t ce = cudaMalloc((void **)&p->mem, p->mem_bytes);
+    // stream-ordered allocation from the device's default pool, retained across plans so a
+    // stream of batches does not pay cudaMalloc/cudaFree each time
+    static bool pool_set[64] = {false};
+    if (!pool_set[p->device]) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, p->device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        pool_set[p->device] = true;
+    }
+    p->stream = st;
+    cudaError_t ce = cudaMallocAsync((void **)&p->mem, p->mem_bytes, st);
     if (ce != cudaSuccess) {
         delete p;
         return fail(DFTB_ERESOURCE, std::string("device allocation of ") + std::to_string(p->mem_bytes >> 20) +
