@@ -25,11 +25,11 @@ void launch_onee(const DevBatch &b, cudaStream_t s);
 void launch_grid(const DevBatch &b, int max_atoms, cudaStream_t s);
 void launch_jk(const DevBatch &b, int nmax, cudaStream_t s);
 int launch_xc(const DevBatch &b, const int *bucket_ctas, const int *bucket_n, int nsh_max, cudaStream_t s);
-void launch_orth(const DevBatch &b, cudaStream_t s);
-void launch_post(const DevBatch &b, int it, int diis_start, int diis_hist, double damping, double conv_std,
-                 cudaStream_t s);
+void launch_orth(const DevBatch &b, int nmax, cudaStream_t s);
+void launch_post(const DevBatch &b, int nmax, int it, int diis_start, int diis_hist, double damping,
+                 double conv_std, cudaStream_t s);
 void launch_reduce(const DevBatch &b, int which, cudaStream_t s);
-void launch_roothaan(const DevBatch &b, cudaStream_t s);
+void launch_roothaan(const DevBatch &b, int nmax, cudaStream_t s);
 void launch_diis_single(const double *F, const double *E, int mh, int n, double *out, cudaStream_t s);
 void launch_eval_ao(const DevBatch &b, int mol, double *out, cudaStream_t s);
 void launch_b3lyp(const double *n, const double *s, int64_t np, double *e, double *vr, double *vs, cudaStream_t st);
@@ -444,9 +444,9 @@ int dftb_plan_begin(dftb_plan *p, void *stream) {
     launch_onee(d, st);
     launch_enn(d, st);
     launch_grid(d, p->natom_max, st);
-    launch_orth(d, st);
+    launch_orth(d, p->nmax, st);
     const dftb_opts &o = p->opts;
-    launch_post(d, -1, o.diis_start, o.diis_history, o.damping_factor, o.convergence_std, st);
+    launch_post(d, p->nmax, -1, o.diis_start, o.diis_history, o.damping_factor, o.convergence_std, st);
     p->launches += 5;
     CK(cudaGetLastError());
     mark(p, 2, st);
@@ -460,7 +460,7 @@ int dftb_plan_iterate(dftb_plan *p, int32_t it, void *stream) {
     const dftb_opts &o = p->opts;
     launch_jk(d, p->nmax, st);
     const int nxl = launch_xc(d, p->xc_bucket_ctas, p->xc_bucket_n, p->nsh_max, st);
-    launch_post(d, it, o.diis_start, o.diis_history, o.damping_factor, o.convergence_std, st);
+    launch_post(d, p->nmax, it, o.diis_start, o.diis_history, o.damping_factor, o.convergence_std, st);
     p->launches += 2 + nxl;
     CK(cudaGetLastError());
     return 0;
@@ -688,9 +688,9 @@ int dftb_plan_roothaan(dftb_plan *p, const double *F_host, double *C_host, doubl
     cudaStream_t st = (cudaStream_t)stream;
     // S must be present (dftb_plan_one_electron or dftb_plan_set "S"); X from S
     CK(cudaMemsetAsync(p->d.status, 0, sizeof(int) * p->d.n_mol, st));
-    launch_orth(p->d, st);
+    launch_orth(p->d, p->nmax, st);
     CK(cudaMemcpyAsync(p->d.F, F_host, sizeof(double) * p->mat0[p->d.n_mol], cudaMemcpyHostToDevice, st));
-    launch_roothaan(p->d, st);
+    launch_roothaan(p->d, p->nmax, st);
     CK(cudaGetLastError());
     if (C_host) CK(cudaMemcpyAsync(C_host, p->d.C, sizeof(double) * p->mat0[p->d.n_mol], cudaMemcpyDeviceToHost, st));
     if (eps_host) CK(cudaMemcpyAsync(eps_host, p->d.eps, sizeof(double) * NMAX * p->d.n_mol, cudaMemcpyDeviceToHost, st));

@@ -13,14 +13,15 @@
 
 namespace dftb {
 
-constexpr int SCF_THREADS = 512;
+constexpr int SCF_THREADS = 256;
 constexpr int KP = 32;  // GEMM K-panel
 
 struct Arena {
-    double *A, *B, *W;  // NMAX*NMAX each; W doubles as GEMM staging and Jacobi's second A buffer
-    double *sa, *sb;    // KP*NMAX each, inside W
-    double *cs, *sn;    // rotations, double-buffered [2][NMAX/2+1]
-    int *pp, *qq;       // rotation pairs [2][NMAX/2+1]
+    int nm;             // arena dimension (largest N of the batch) and staging leading dim
+    double *A, *B, *W;  // nm*nm each (W >= 2*KP*nm); W doubles as GEMM staging and Jacobi's 2nd A
+    double *sa, *sb;    // KP*nm each, inside W
+    double *cs, *sn;    // rotations, double-buffered [2][NPH]
+    int *pp, *qq;       // rotation pairs [2][NPH]
     int *pos;           // index -> 2*pair + is_q, [2][NMAX+2]
     int *perm;          // [NMAX]
     double *dv;         // [NMAX]
@@ -32,14 +33,17 @@ struct Arena {
 
 constexpr int NPH = NMAX / 2 + 1;
 
-__device__ __forceinline__ Arena carve(unsigned char *base) {
+HD size_t arena_w(int nm) { return (size_t)(nm * nm > 2 * KP * nm ? nm * nm : 2 * KP * nm); }
+
+__device__ __forceinline__ Arena carve(unsigned char *base, int nm) {
     Arena a;
+    a.nm = nm;
     double *p = (double *)base;
-    a.A = p; p += NMAX * NMAX;
-    a.B = p; p += NMAX * NMAX;
-    a.W = p; p += NMAX * NMAX;
+    a.A = p; p += nm * nm;
+    a.B = p; p += nm * nm;
+    a.W = p; p += arena_w(nm);
     a.sa = a.W;
-    a.sb = a.W + KP * NMAX;
+    a.sb = a.W + KP * nm;
     a.cs = p; p += 2 * NPH;
     a.sn = p; p += 2 * NPH;
     a.dv = p; p += NMAX;
@@ -55,8 +59,8 @@ __device__ __forceinline__ Arena carve(unsigned char *base) {
     return a;
 }
 
-size_t scf_smem_bytes() {
-    return sizeof(double) * (3 * NMAX * NMAX + 4 * NPH + NMAX + 100 + 10 + 32 + 16) +
+size_t scf_smem_bytes(int nm) {
+    return sizeof(double) * (2 * (size_t)nm * nm + arena_w(nm) + 4 * NPH + NMAX + 100 + 10 + 32 + 16) +
            sizeof(int) * (4 * NPH + 2 * (NMAX + 2) + NMAX);
 }
 
@@ -64,48 +68,49 @@ size_t scf_smem_bytes() {
 // Operands may live in global or shared memory; M, N <= NMAX.
 __device__ void cta_gemm(double *C, int ldc, const double *A, int lda, bool tA, const double *B, int ldb,
                          bool tB, int M, int N, int K, double alpha, double beta, const Arena &ar) {
-    const int tid = threadIdx.x, ty = tid >> 5, tx = tid & 31;  // 16 x 32 threads
-    double acc[6][3];
+    const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;  // 16 x 16 threads, 6 x 6 tiles
+    const int LD = ar.nm;
+    double acc[6][6];
 #pragma unroll
     for (int a = 0; a < 6; ++a)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) acc[a][c] = 0.0;
+        for (int c = 0; c < 6; ++c) acc[a][c] = 0.0;
     for (int k0 = 0; k0 < K; k0 += KP) {
         const int kn = min(KP, K - k0);
         // staging loops map consecutive threads to the operand's contiguous index (coalesced)
-        for (int t = tid; t < KP * NMAX; t += SCF_THREADS) {
+        for (int t = tid; t < KP * LD; t += SCF_THREADS) {
             int kk, i;
-            if (tA) { kk = t / NMAX; i = t % NMAX; } else { i = t / KP; kk = t % KP; }
+            if (tA) { kk = t / LD; i = t - kk * LD; } else { i = t / KP; kk = t - i * KP; }
             double va = 0.0;
             if (kk < kn && i < M) va = tA ? A[(int64_t)(k0 + kk) * lda + i] : A[(int64_t)i * lda + k0 + kk];
-            ar.sa[kk * NMAX + i] = va;
+            ar.sa[kk * LD + i] = va;
         }
-        for (int t = tid; t < KP * NMAX; t += SCF_THREADS) {
+        for (int t = tid; t < KP * LD; t += SCF_THREADS) {
             int kk, j;
-            if (!tB) { kk = t / NMAX; j = t % NMAX; } else { j = t / KP; kk = t % KP; }
+            if (!tB) { kk = t / LD; j = t - kk * LD; } else { j = t / KP; kk = t - j * KP; }
             double vb = 0.0;
             if (kk < kn && j < N) vb = tB ? B[(int64_t)j * ldb + k0 + kk] : B[(int64_t)(k0 + kk) * ldb + j];
-            ar.sb[kk * NMAX + j] = vb;
+            ar.sb[kk * LD + j] = vb;
         }
         __syncthreads();
         for (int kk = 0; kk < kn; ++kk) {
-            double av[6], bv[3];
+            double av[6], bv[6];
 #pragma unroll
-            for (int a = 0; a < 6; ++a) av[a] = ar.sa[kk * NMAX + ty + 16 * a];
+            for (int a = 0; a < 6; ++a) av[a] = (ty + 16 * a < LD) ? ar.sa[kk * LD + ty + 16 * a] : 0.0;
 #pragma unroll
-            for (int c = 0; c < 3; ++c) bv[c] = ar.sb[kk * NMAX + tx + 32 * c];
+            for (int c = 0; c < 6; ++c) bv[c] = (tx + 16 * c < LD) ? ar.sb[kk * LD + tx + 16 * c] : 0.0;
 #pragma unroll
             for (int a = 0; a < 6; ++a)
 #pragma unroll
-                for (int c = 0; c < 3; ++c) acc[a][c] = fma(av[a], bv[c], acc[a][c]);
+                for (int c = 0; c < 6; ++c) acc[a][c] = fma(av[a], bv[c], acc[a][c]);
         }
         __syncthreads();
     }
 #pragma unroll
     for (int a = 0; a < 6; ++a)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const int i = ty + 16 * a, j = tx + 32 * c;
+        for (int c = 0; c < 6; ++c) {
+            const int i = ty + 16 * a, j = tx + 16 * c;
             if (i < M && j < N) {
                 double v = alpha * acc[a][c];
                 if (beta != 0.0) v += beta * C[(int64_t)i * ldc + j];
@@ -154,14 +159,16 @@ __device__ double *cta_jacobi(double *A0, double *A1, double *V, int n, const Ar
         else task[s] = -1;
     }
     double *cur = A0, *nxt = A1;
+    const int kr = tid;
+    const bool rot_owner = tid < np;
     // rotations of global step 0 from cur directly (buffer 0)
-    if (tid < np) {
+    if (rot_owner) {
         int p, q;
-        jac_pair(tid, 0, n2, p, q);
+        jac_pair(kr, 0, n2, p, q);
         double c = 1.0, sn = 0.0;
         if (q < n) jac_angle(cur[p * n + p], cur[q * n + q], cur[p * n + q], c, sn);
-        ar.cs[tid] = c; ar.sn[tid] = sn; ar.pp[tid] = p; ar.qq[tid] = q;
-        ar.pos[p] = 2 * tid; ar.pos[q] = 2 * tid + 1;
+        ar.cs[kr] = c; ar.sn[kr] = sn; ar.pp[kr] = p; ar.qq[kr] = q;
+        ar.pos[p] = 2 * kr; ar.pos[q] = 2 * kr + 1;
     }
     __syncthreads();
     int sweeps = 0;
@@ -185,10 +192,10 @@ __device__ double *cta_jacobi(double *A0, double *A1, double *V, int n, const Ar
         }
         const double *cs = ar.cs + bf * NPH, *sn = ar.sn + bf * NPH;
         const int *pp = ar.pp + bf * NPH, *qq = ar.qq + bf * NPH, *pos = ar.pos + bf * (NMAX + 2);
-        if (tid < np) {  // angles for step g+1 from cur and this step's rotations
+        if (rot_owner) {  // angles for step g+1 from cur and this step's rotations
             const int r1 = (g + 1) % R;
             int p, q;
-            jac_pair(tid, r1, n2, p, q);
+            jac_pair(kr, r1, n2, p, q);
             double c = 1.0, s1 = 0.0;
             if (q < n) {
                 // element (x, y) of J^T cur J
@@ -207,9 +214,9 @@ __device__ double *cta_jacobi(double *A0, double *A1, double *V, int n, const Ar
                 };
                 jac_angle(el(p, p), el(q, q), el(p, q), c, s1);
             }
-            ar.cs[nb * NPH + tid] = c; ar.sn[nb * NPH + tid] = s1;
-            ar.pp[nb * NPH + tid] = p; ar.qq[nb * NPH + tid] = q;
-            ar.pos[nb * (NMAX + 2) + p] = 2 * tid; ar.pos[nb * (NMAX + 2) + q] = 2 * tid + 1;
+            ar.cs[nb * NPH + kr] = c; ar.sn[nb * NPH + kr] = s1;
+            ar.pp[nb * NPH + kr] = p; ar.qq[nb * NPH + kr] = q;
+            ar.pos[nb * (NMAX + 2) + p] = 2 * kr; ar.pos[nb * (NMAX + 2) + q] = 2 * kr + 1;
         }
 #pragma unroll
         for (int s = 0; s < JAC_MAXT; ++s) {
@@ -264,9 +271,9 @@ __device__ void sort_eigs(const double *A, int n, const Arena &ar) {
 }
 
 // ---------------------------------------------------------------------------- orthogonaliser
-__global__ void __launch_bounds__(SCF_THREADS) k_orth(DevBatch b) {
+__global__ void __launch_bounds__(SCF_THREADS, 2) k_orth(DevBatch b, int nm) {
     extern __shared__ __align__(16) unsigned char ssm[];
-    const Arena ar = carve(ssm);
+    const Arena ar = carve(ssm, nm);
     const int m = blockIdx.x, N = b.m_nao[m], tid = threadIdx.x;
     const int64_t o = b.m_mat0[m];
     for (int t = tid; t < N * N; t += SCF_THREADS) {
@@ -389,6 +396,7 @@ void launch_reduce(const DevBatch &b, int which, cudaStream_t s) {
 
 // ---------------------------------------------------------------------------- post kernel
 struct PostArgs {
+    int nm;             // arena dimension
     int it;             // iteration index; -1 = core-Hamiltonian guess
     int diis_start, diis_hist;
     double damping, conv_std;
@@ -468,9 +476,9 @@ __device__ void diis_extrapolate(const DevBatch &b, int m, int N, const double *
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(SCF_THREADS) k_post(DevBatch b, PostArgs pa) {
+__global__ void __launch_bounds__(SCF_THREADS, 2) k_post(DevBatch b, PostArgs pa) {
     extern __shared__ __align__(16) unsigned char ssm[];
-    const Arena ar = carve(ssm);
+    const Arena ar = carve(ssm, pa.nm);
     const int m = blockIdx.x, tid = threadIdx.x;
     if (b.done[m]) return;
     const int N = b.m_nao[m], M = b.nmo[m], nocc = b.m_nocc[m];
@@ -612,25 +620,29 @@ __global__ void __launch_bounds__(SCF_THREADS) k_post(DevBatch b, PostArgs pa) {
     }
 }
 
-void launch_orth(const DevBatch &b, cudaStream_t s) {
-    const size_t sm = scf_smem_bytes();
+static int arena_dim(int nmax) { return nmax < 16 ? 16 : nmax; }
+
+void launch_orth(const DevBatch &b, int nmax, cudaStream_t s) {
+    const int nm = arena_dim(nmax);
+    const size_t sm = scf_smem_bytes(nm);
     cudaFuncSetAttribute(k_orth, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_orth<<<b.n_mol, SCF_THREADS, sm, s>>>(b);
+    k_orth<<<b.n_mol, SCF_THREADS, sm, s>>>(b, nm);
 }
 
-void launch_post(const DevBatch &b, int it, int diis_start, int diis_hist, double damping, double conv_std,
-                 cudaStream_t s) {
-    const size_t sm = scf_smem_bytes();
+void launch_post(const DevBatch &b, int nmax, int it, int diis_start, int diis_hist, double damping,
+                 double conv_std, cudaStream_t s) {
+    const int nm = arena_dim(nmax);
+    const size_t sm = scf_smem_bytes(nm);
     cudaFuncSetAttribute(k_post, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    PostArgs pa{it, diis_start, diis_hist, damping, conv_std};
+    PostArgs pa{nm, it, diis_start, diis_hist, damping, conv_std};
     k_post<<<b.n_mol, SCF_THREADS, sm, s>>>(b, pa);
 }
 
 // ---------------------------------------------------------------------------- standalone roothaan
 // For the operator-level API: F given per molecule in b.F; writes C, eps (cold Jacobi).
-__global__ void __launch_bounds__(SCF_THREADS) k_roothaan(DevBatch b) {
+__global__ void __launch_bounds__(SCF_THREADS) k_roothaan(DevBatch b, int nm) {
     extern __shared__ __align__(16) unsigned char ssm[];
-    const Arena ar = carve(ssm);
+    const Arena ar = carve(ssm, nm);
     const int m = blockIdx.x, tid = threadIdx.x;
     const int N = b.m_nao[m], M = b.nmo[m];
     const int64_t o = b.m_mat0[m], tot = b.m_mat0[b.n_mol];
@@ -648,10 +660,11 @@ __global__ void __launch_bounds__(SCF_THREADS) k_roothaan(DevBatch b) {
     cta_gemm(C, N, X, N, false, Cp, M, false, N, M, M, 1.0, 0.0, ar);
 }
 
-void launch_roothaan(const DevBatch &b, cudaStream_t s) {
-    const size_t sm = scf_smem_bytes();
+void launch_roothaan(const DevBatch &b, int nmax, cudaStream_t s) {
+    const int nm = arena_dim(nmax);
+    const size_t sm = scf_smem_bytes(nm);
     cudaFuncSetAttribute(k_roothaan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_roothaan<<<b.n_mol, SCF_THREADS, sm, s>>>(b);
+    k_roothaan<<<b.n_mol, SCF_THREADS, sm, s>>>(b, nm);
 }
 
 // ---------------------------------------------------------------------------- standalone DIIS
@@ -659,7 +672,7 @@ void launch_roothaan(const DevBatch &b, cudaStream_t s) {
 __global__ void __launch_bounds__(SCF_THREADS) k_diis_single(const double *F, const double *E, int mh, int n,
                                                             double *out) {
     extern __shared__ __align__(16) unsigned char ssm[];
-    const Arena ar = carve(ssm);
+    const Arena ar = carve(ssm, max(mh + 1, 16));
     const int tid = threadIdx.x, nn = n * n;
     if (mh == 1) {
         for (int t = tid; t < nn; t += SCF_THREADS) out[t] = F[t];
@@ -723,7 +736,7 @@ __global__ void __launch_bounds__(SCF_THREADS) k_diis_single(const double *F, co
 }
 
 void launch_diis_single(const double *F, const double *E, int mh, int n, double *out, cudaStream_t s) {
-    const size_t sm = scf_smem_bytes();
+    const size_t sm = scf_smem_bytes(max(mh + 1, 16));
     cudaFuncSetAttribute(k_diis_single, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k_diis_single<<<1, SCF_THREADS, sm, s>>>(F, E, mh, n, out);
 }
