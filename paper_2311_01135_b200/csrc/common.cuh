@@ -21,13 +21,33 @@ constexpr int NCLS = 6;              // quartet classes (LL|LL) (LL|LS) (LL|SS) 
 
 HD int64_t tri(int64_t i) { return i * (i + 1) / 2; }
 HD int64_t pidx(int i, int j) { return i >= j ? tri(i) + j : tri(j) + i; }
-// ERI store rows are padded to 16 bytes (g elements: 4 for f32, 2 for f64) so every row
-// can be fetched with one cp.async.bulk.  Row P (P+1 entries) starts at rowbase(P, g).
-HD int64_t rowpad(int64_t len, int g) { return (len + g - 1) / g * g; }
-HD int64_t rowbase(int64_t P, int g) {
-    const int64_t a = P / g, r = P % g;
-    return (int64_t)g * (g * a * (a + 1) / 2 + r * (a + 1));
+// ERI store layout ("ket-tiled rows").  Row P = (i, j), i >= j, holds the kets (k, l),
+// k >= l, (k, l) <= (i, j) as the lower-triangular 4x4 tiles of its symmetric ket matrix
+// restricted to k, l <= i: tile (a, b), a >= b, a <= i/4, sits at tile index tri(a) + b,
+// 16 elements [k%4][l%4].  Slots with l > k inside diagonal tiles, with k > i, or with
+// k == i and l > j are zero (they belong to other rows).  All i + 1 rows of slab i have the
+// same length 16 * tri(i/4 + 1), so a row starts on a 64-byte (f32) / 128-byte (f64)
+// boundary and the J/K kernel can read whole tiles with 16-byte vector loads.
+HD int64_t eri_rowlen(int i) {
+    const int64_t A = (i >> 2) + 1;
+    return 8 * A * (A + 1);
 }
+HD int64_t eri_slab0(int i) {                 // elements in all rows with first index < i
+    const int64_t a = i >> 2;
+    const int64_t h = a * (a - 1) / 2;
+    const int64_t full = 8 * (16 * h * h + 58 * ((a - 1) * a * (2 * a - 1) / 6) + 62 * h + 20 * a);
+    return full + eri_rowlen(i) * (tri(i) - tri(4 * a));
+}
+HD int64_t eri_row(int i, int j) { return eri_slab0(i) + (int64_t)j * eri_rowlen(i); }
+HD int eri_ket(int k, int l) { return 16 * (int)(tri(k >> 2) + (l >> 2)) + 4 * (k & 3) + (l & 3); }  // k >= l
+// offset of (ij|kl) in a molecule's store (any index order)
+HD int64_t eri_pos(int i, int j, int k, int l) {
+    if (i < j) { const int t = i; i = j; j = t; }
+    if (k < l) { const int t = k; k = l; l = t; }
+    if (tri(i) + j < tri(k) + l) { int t = i; i = k; k = t; t = j; j = l; l = t; }
+    return eri_row(i, j) + eri_ket(k, l);
+}
+HD int64_t eri_size(int N) { return eri_slab0(N); }
 
 // Device-resident view of one batch.  Every pointer is a device pointer owned by
 // the plan (plan.cu).  Index conventions: "global" = over the whole batch,

@@ -111,9 +111,7 @@ __device__ __forceinline__ void load_geo(const DevBatch &b, int64_t pr, double *
 
 template <typename ST>
 __device__ __forceinline__ void store_eri(ST *eri, int64_t base, int i, int j, int k, int l, double v) {
-    int64_t P = pidx(i, j), Q = pidx(k, l);
-    if (P < Q) { int64_t t = P; P = Q; Q = t; }
-    eri[base + rowbase(P, 16 / (int)sizeof(ST)) + Q] = (ST)v;
+    eri[base + eri_pos(i, j, k, l)] = (ST)v;
 }
 
 // --------------------------------------------------------------------------- ERI kernels

@@ -1,38 +1,46 @@
-// J/K digestion over the dense 8-fold ERI store — deterministic, no atomics.
+// J/K digestion over the ket-tiled ERI store — deterministic, no atomics.
 //
 // Reference: deskdft.integrals.build_jk (integrals.py:199-218) -> _jk_kernel
 // (_kernels.py:650-693), which scatters each canonical entry to its <= 8 images.
 //
-// B200 formulation ("row owner"): a CTA owns the store rows P = (i, j), j <= i,
-// for one or two values of i.  Row P holds (ij|kl) for all Q = (k, l) <= P.  For a
-// stored element the 8 images contribute J_P += v rho~_Q, J_Q += v rho~_P and —
-// recording each K contribution at (a,d) or its transpose — only G[i][.] and G[j][.]
-// updates (K = -(G + G^T)/4 at the end).  Per row the CTA computes two GEMVs with
-// the row's symmetric ket matrix T (T rho_j, T rho_i), read straight from the
-// staged packed row, and one dot product.  G_i accumulates in registers across the
-// CTA's rows, the J_Q scatter accumulates in registers (thread t owns Q = t mod
-// 256), G_j rows and J partials are written once and summed in a fixed order by the
-// SCF post kernel.  One CTA barrier per row.
+// B200 formulation.  The store row P = (i, j) is the lower half of the symmetric ket
+// matrix T_P (k, l <= i) in 4x4 tiles (common.cuh, "ket-tiled rows").  For a stored
+// element the 8 images contribute J_P += v rho~_Q, J_Q += v rho~_P and — recording each
+// K contribution at (a,d) or its transpose — only rows i and j of an intermediate G
+// (K = -(G + G^T)/4 in the post kernel):
+//     G_i += 2 T_P rho_j - c,   G_j = 2 T_P rho_i - c'   (c, c' = the (ij|ij) element's
+//                                                      second image, subtracted once)
+// A CTA owns a contiguous range of whole slabs i (all rows (i, .)), streamed in chunks of
+// CR (= 4) consecutive rows by cp.async.bulk (TMA bulk copy, mbarrier completion) into a
+// double-buffered shared-memory stage while the previous chunk is digested.  One warp
+// digests one row.  With A = i/4 + 1 the 4-row blocks of the result vectors are paired
+// (a1 = p, a2 = A-1-p); a pair is owned by S lanes, and for each of its two blocks they
+// read the tiles of the block row (row part, T[a][b] rho[b]) and the block column (column
+// part, T[a'][a]^T rho[a']).  Every pair then visits exactly A + 1 tiles in each of the two
+// loops (no divergence between lanes); the S lanes split the tiles and are combined by a
+// shuffle tree.  Diagonal tiles are used with their diagonal halved (in registers), which
+// makes row part + column part the full symmetric product and gives the J_P dot product a
+// uniform weight of 2.  G_i accumulates in registers over the slab's rows; the scattered
+// J_Q contributions are a second sweep over the staged chunk with thread-owned 16-byte
+// units, so they accumulate in registers across the CTA's whole slab range.  All products
+// are formed in f64; every output is written once and summed in a fixed order by the
+// post kernel.
 //
-// Data movement: rows are 16-byte padded in HBM and prefetched whole with
-// cp.async.bulk (TMA bulk copy, mbarrier completion) into a double-buffered
-// staging area while the previous row is being digested; the store is streamed
-// exactly once per SCF iteration.  In the f32 build rho is kept in f32 shared
-// memory (it is f32-valued there); products are always formed in f64.
+// Algorithmic traffic: the store is read exactly once from HBM per SCF iteration.  Work per
+// stored element: 4 DFMA for K (two visits x (rho_i, rho_j)), 1 for J_P, 1 for J_Q.
 #include "common.cuh"
 
 namespace dftb {
 
-constexpr int JK_THREADS = 256;
-constexpr int JK_NREG = (NMAX * (NMAX + 1) / 2 + JK_THREADS - 1) / JK_THREADS;  // owned J_Q slots
 
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
+constexpr int JK_WARPS = 4;                    // one store row per warp
+constexpr int JK_THREADS = 32 * JK_WARPS;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
-__device__ __forceinline__ void bulk_row(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+__device__ __forceinline__ void bulk_copy(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
     asm volatile(
@@ -51,212 +59,312 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
-constexpr int JK_R = 4;                  // rows per chunk (one TMA bulk copy)
-constexpr int JK_G = JK_THREADS / JK_R;  // threads per row (64)
-
-struct JKLayout {
-    size_t stage, rho, lut, gpart, total;
-    int64_t chunk;                        // elements per staging buffer
-};
-
 template <typename ST>
-HD JKLayout jk_layout(int N, int nbuf) {
-    const int g = 16 / (int)sizeof(ST);
-    const int64_t npp = (int64_t)N * (N + 1) / 2;
-    JKLayout L;
-    L.chunk = (int64_t)JK_R * rowpad(npp, g);
-    size_t o = 64;                                    // mbarriers
-    L.stage = o; o += (size_t)nbuf * L.chunk * sizeof(ST);
-    o = (o + 15) & ~(size_t)15;
-    L.rho = o; o += (size_t)N * N * sizeof(double);
-    L.lut = o; o += (size_t)npp * sizeof(uint16_t);
-    o = (o + 15) & ~(size_t)15;
-    L.gpart = o; o += (size_t)JK_R * 2 * JK_G * sizeof(double);
-    L.total = o;
-    return L;
+__device__ __forceinline__ void tile_ld(const ST *p, double (&t)[16]) {
+    if constexpr (sizeof(ST) == 4) {
+        const float4 *q = reinterpret_cast<const float4 *>(p);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const float4 v = q[r];
+            t[4 * r] = v.x; t[4 * r + 1] = v.y; t[4 * r + 2] = v.z; t[4 * r + 3] = v.w;
+        }
+    } else {
+        const double2 *q = reinterpret_cast<const double2 *>(p);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const double2 v = q[r];
+            t[2 * r] = v.x; t[2 * r + 1] = v.y;
+        }
+    }
 }
 
-// A CTA digests the rows P = (i, j) of one or two i-slabs in chunks of JK_R consecutive
-// rows (contiguous in HBM -> one cp.async.bulk per chunk, double buffered).  Within a
-// chunk, 64 threads per row form the J_P dot product and the two K GEMVs with the
-// row's symmetric ket matrix T, read straight from the staged packed row:
-//   element (k, l) sits at tri(k) + l, so column t of T is row[tri(t) + n] (n < t) and
-//   row[tri(n) + t] (n >= t); a single merged walk over n keeps every lane busy.
-// The scattered J_Q contributions are done column-wise per chunk by the thread that owns
-// Q (Q = tid mod 256), so they accumulate in registers across the CTA's rows.
-template <typename ST>
-__global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, int nbuf) {
-    extern __shared__ __align__(128) unsigned char sm[];
-    const int cta = blockIdx.x;
+__device__ __forceinline__ void ld4(const double *p, double (&v)[4]) {
+    const double2 a = *reinterpret_cast<const double2 *>(p);
+    const double2 c = *reinterpret_cast<const double2 *>(p + 2);
+    v[0] = a.x; v[1] = a.y; v[2] = c.x; v[3] = c.y;
+}
+
+__device__ __forceinline__ double shfl_x(double v, int o) { return __shfl_xor_sync(0xffffffffu, v, o); }
+
+// Shared-memory plan of one bucket: NBUF staging buffers of CR rows, padded rho, G_i
+// reduction scratch.  Double buffering (then rows per chunk) is reduced for the largest
+// buckets to fit 227 KB.
+template <typename ST, int NB>
+struct JKPlan {
+    static constexpr int AMAX = NB / 4;
+    static constexpr int LMAX = 8 * AMAX * (AMAX + 1);
+    static constexpr size_t row_bytes = (size_t)LMAX * sizeof(ST);
+    static constexpr size_t fixed = 128 + sizeof(double) * ((size_t)NB * NB + 8 * JK_THREADS);
+    static constexpr size_t cap = 227 * 1024;
+    static constexpr int NBUF = fixed + 2 * JK_WARPS * row_bytes <= cap ? 2 : 1;
+    static constexpr int CR = fixed + NBUF * JK_WARPS * row_bytes <= cap ? JK_WARPS : JK_WARPS / 2;
+    static constexpr size_t bytes = fixed + NBUF * CR * row_bytes;
+    static_assert(bytes <= 227 * 1024, "J/K bucket does not fit in shared memory");
+};
+
+// rho in shared memory: row-major with stride NP, 16-byte chunks XOR-swizzled by the row's
+// 4-block so that the lanes of a warp (different blocks a, same column block) hit
+// different banks.
+template <int NP>
+__device__ __forceinline__ int rsw(int r, int c) {
+    static_assert(NP % 16 == 0, "chunk swizzle needs NP / 2 to be a multiple of 8");
+    return r * NP + (((c >> 1) ^ ((r >> 2) & 7)) << 1) + (c & 1);
+}
+template <int NP>
+__device__ __forceinline__ void ld4r(const double *rho, int r, int c4, double (&v)[4]) {   // c4 % 4 == 0
+    const double2 a = *reinterpret_cast<const double2 *>(rho + rsw<NP>(r, c4));
+    const double2 c = *reinterpret_cast<const double2 *>(rho + rsw<NP>(r, c4 + 2));
+    v[0] = a.x; v[1] = a.y; v[2] = c.x; v[3] = c.y;
+}
+
+// NB: AO-count bound of the bucket (multiple of 16) — fixes the padded rho stride, the
+// staging size and the number of J_Q units each thread owns.
+template <typename ST, int NB>
+__global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, const int *ctas) {
+    using PL = JKPlan<ST, NB>;
+    constexpr int VW = 16 / (int)sizeof(ST);                   // elements per 16-byte unit
+    constexpr int LMAX = PL::LMAX, NBUF = PL::NBUF, CR = PL::CR;
+    constexpr int KU = (LMAX / VW + JK_THREADS - 1) / JK_THREADS;
+    constexpr int NP = NB;                                      // padded rho stride
+    extern __shared__ __align__(128) unsigned char jsm[];
+    uint64_t *bar = (uint64_t *)jsm;
+    double *rho = (double *)(jsm + 128);                        // [NP][NP] swizzled, zero padded
+    double *gred = rho + NP * NP;                               // [JK_THREADS][8]
+    ST *stage = (ST *)(gred + 8 * JK_THREADS);                  // [NBUF][CR * LMAX]
+    const int cta = ctas[blockIdx.x];
     const int m = b.jk_mol[cta];
     if (b.done[m]) return;
     const int N = b.m_nao[m];
-    const int g = 16 / (int)sizeof(ST);
     const int64_t npp = tri(N);
-    const JKLayout L = jk_layout<ST>(N, nbuf);
-    uint64_t *bar = (uint64_t *)sm;
-    ST *stage = (ST *)(sm + L.stage);
-    double *rho = (double *)(sm + L.rho);
-    uint16_t *lut = (uint16_t *)(sm + L.lut);
-    double *gpart = (double *)(sm + L.gpart);
-    const int tid = threadIdx.x;
-    const int grp = tid / JK_G, gt = tid % JK_G;      // row slot in the chunk, thread in the row
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
     const ST *eri = (const ST *)b.eri + b.m_eri0[m];
-    const int iv[2] = {b.jk_i0[cta], b.jk_i1[cta]};
-    // chunk list: (slab s, first j); nch0 chunks for the first slab
-    const int nch0 = (iv[0] + JK_R) / JK_R;
-    const int nch = nch0 + (iv[1] >= 0 ? (iv[1] + JK_R) / JK_R : 0);
-    auto chunk_of = [&](int c, int &i, int &j0, int &nr) {
-        const int s = c < nch0 ? 0 : 1, cc = c < nch0 ? c : c - nch0;
-        i = iv[s];
-        j0 = cc * JK_R;
-        nr = min(JK_R, i + 1 - j0);
-    };
-    auto issue = [&](int c) {
-        int i, j0, nr;
-        chunk_of(c, i, j0, nr);
-        const int64_t P0 = tri(i) + j0;
-        const int64_t e0 = rowbase(P0, g), e1 = rowbase(P0 + nr, g);
-        bulk_row(stage + (c % nbuf) * L.chunk, eri + e0, (uint32_t)((e1 - e0) * sizeof(ST)), bar + (c % nbuf));
+    const int i0 = b.jk_i0[cta], i1 = b.jk_i1[cta];
+    // chunk producer (thread 0): chunks = CR consecutive rows of one slab, slabs walked
+    // from i1-1 down to i0
+    int pi = i1 - 1, pj = 0;
+    auto issue = [&](int slot) {
+        const int nr = min(CR, pi + 1 - pj);
+        const int64_t L = eri_rowlen(pi);
+        bulk_copy(stage + (size_t)slot * CR * LMAX, eri + eri_row(pi, pj),
+                  (uint32_t)(nr * L * sizeof(ST)), bar + slot);
+        pj += CR;
+        if (pj > pi) { --pi; pj = 0; }
     };
     if (tid == 0) {
-        for (int k = 0; k < nbuf; ++k) mbar_init(bar + k, 1);
+        for (int k = 0; k < NBUF; ++k) mbar_init(bar + k, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int k = 0; k < NBUF && pi >= i0; ++k) issue(k);
+    }
+    const double *rg = b.rho + b.m_mat0[m];
+    for (int t = tid; t < NP * NP; t += JK_THREADS) {
+        const int r = t / NP, c = t % NP;
+        rho[rsw<NP>(r, c)] = (r < N && c < N) ? rg[r * N + c] : 0.0;
     }
     __syncthreads();
-    if (tid == 0)
-        for (int c = 0; c < nbuf && c < nch; ++c) issue(c);
-    const double *rg = b.rho + b.m_mat0[m];
-    for (int t = tid; t < N * N; t += JK_THREADS) rho[t] = rg[t];
-    for (int k = tid; k < N; k += JK_THREADS)
-        for (int l = 0; l <= k; ++l) lut[tri(k) + l] = (uint16_t)((k << 8) | l);
-    __syncthreads();
-    double jsc[JK_NREG];
+    double acc[KU][VW];
 #pragma unroll
-    for (int q = 0; q < JK_NREG; ++q) jsc[q] = 0.0;
+    for (int k = 0; k < KU; ++k)
+#pragma unroll
+        for (int v = 0; v < VW; ++v) acc[k][v] = 0.0;
     double *Gp = b.Gpart + b.m_G0[m];
     double *Jp = b.Jpart + b.m_Jp0[m];
-    double gi0 = 0.0, gi1 = 0.0;                      // G_i[t] partials, t = gt and gt + 64
-    for (int c = 0; c < nch; ++c) {
-        int i, j0, nr;
-        chunk_of(c, i, j0, nr);
-        const int64_t P0 = tri(i) + j0;
-        const ST *cbuf = stage + (c % nbuf) * L.chunk;
-        mbar_wait(bar + (c % nbuf), (uint32_t)((c / nbuf) & 1));
-        const int64_t rb0 = rowbase(P0, g);
-        if (grp < nr) {
-            const int j = j0 + grp;
-            const int P = (int)(P0 + grp);
-            const ST *row = cbuf + (rowbase(P, g) - rb0);
-            // ---- J_P = sum_Q v_PQ rho~_Q  (64 threads, fixed shuffle tree + smem pair sum)
-            double jown = 0.0;
-            for (int e = gt; e <= P; e += JK_G) {
-                const int kl = lut[e], k = kl >> 8, l = kl & 255;
-                jown += (double)row[e] * rho[k * N + l] * (k != l ? 2.0 : 1.0);
-            }
-            jown = warp_sum(jown);
-            // ---- K: G_i[t] += (T rho_j)[t], G_j[t] = (T rho_i)[t]
-            const double *rj = rho + j * N, *ri = rho + i * N;
+    int chunk = 0;
+    for (int i = i1 - 1; i >= i0; --i) {
+        const int A = (i >> 2) + 1;
+        // lanes: S per 4-block a of the result vectors, block a = lane / S
+        const int S = A <= 1 ? 32 : A <= 2 ? 16 : A <= 4 ? 8 : A <= 8 ? 4 : A <= 16 ? 2 : 1;
+        const int a = lane / S, s = lane % S;
+        const bool lane_ok = a < A;
+        const int64_t L = eri_rowlen(i);
+        const int units = (int)(L / VW);
+        double gi[4] = {0, 0, 0, 0};
+        for (int j0 = 0; j0 <= i; j0 += CR, ++chunk) {
+            const int slot = chunk % NBUF;
+            const ST *cbuf = stage + (size_t)slot * CR * LMAX;
+            mbar_wait(bar + slot, (uint32_t)((chunk / NBUF) & 1));
+            const int j = j0 + w;
+            if (w < CR && j <= i) {                    // warp-uniform
+                const ST *row = cbuf + (int64_t)w * L;
+                double oI[4] = {0, 0, 0, 0}, oJ[4] = {0, 0, 0, 0}, jp = 0.0;
+                if (lane_ok) {
+                    // block a: row part tiles (a, q), q = 0..a, then column part tiles
+                    // (q-1, a), q = a+1..A (transposed); A + 1 tiles for every block
+                    for (int q = s; q <= A; q += S) {
+                        const bool rp = q <= a;
+                        const int ta = rp ? a : q - 1, tb = rp ? q : a;   // tile (ta, tb)
+                        const int beta = rp ? q : q - 1;                  // rho block of the product
+                        float tf[16];
+                        {
+                            const float4 *qp = reinterpret_cast<const float4 *>(row + 16 * (tri(ta) + tb));
+                            if constexpr (sizeof(ST) == 4) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int t = gt + h * JK_G;
-                if (t > i) break;
-                const int tt = (int)tri(t);
-                double ai = 0.0, aj = 0.0;
-                int trin = 0;                         // tri(n)
-                for (int n = 0; n <= i; ++n) {
-                    const int e = n < t ? tt + n : trin + t;
-                    trin += n + 1;
-                    if (e <= P) {
-                        const double v = (double)row[e];
-                        ai += v * rj[n];
-                        aj += v * ri[n];
+                                for (int r = 0; r < 4; ++r) {
+                                    const float4 v = qp[r];
+                                    tf[4 * r] = v.x; tf[4 * r + 1] = v.y; tf[4 * r + 2] = v.z; tf[4 * r + 3] = v.w;
+                                }
+                            }
+                        }
+                        double t[16];
+                        if constexpr (sizeof(ST) == 4) {
+#pragma unroll
+                            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                                for (int c = 0; c < 4; ++c)
+                                    t[4 * r + c] = (double)(rp ? tf[4 * r + c] : tf[4 * c + r]);
+                        } else {
+                            double td[16];
+                            const double2 *qp = reinterpret_cast<const double2 *>(row + 16 * (tri(ta) + tb));
+#pragma unroll
+                            for (int r = 0; r < 8; ++r) {
+                                const double2 v = qp[r];
+                                td[2 * r] = v.x; td[2 * r + 1] = v.y;
+                            }
+#pragma unroll
+                            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                                for (int c = 0; c < 4; ++c) t[4 * r + c] = rp ? td[4 * r + c] : td[4 * c + r];
+                        }
+                        if (ta == tb) { t[0] *= 0.5; t[5] *= 0.5; t[10] *= 0.5; t[15] *= 0.5; }
+                        double jv[4], iv[4];
+                        ld4r<NP>(rho, j, 4 * beta, jv);
+                        ld4r<NP>(rho, i, 4 * beta, iv);
+                        const double jw = rp ? 1.0 : 0.0;      // J_P: row-part tiles only
+#pragma unroll
+                        for (int rr = 0; rr < 4; ++rr) {
+                            double x[4];
+                            ld4r<NP>(rho, 4 * a + rr, 4 * beta, x);
+                            double d = 0.0;
+#pragma unroll
+                            for (int cc = 0; cc < 4; ++cc) {
+                                oJ[rr] = fma(t[4 * rr + cc], jv[cc], oJ[rr]);
+                                oI[rr] = fma(t[4 * rr + cc], iv[cc], oI[rr]);
+                                d = fma(t[4 * rr + cc], x[cc], d);
+                            }
+                            jp = fma(jw, d, jp);
+                        }
                     }
                 }
-                // T = 2 v except the row's own element (weight 1): corrected once
-                ai *= 2.0;
-                aj *= 2.0;
-                const double vp = (double)row[P];
-                if (t == j) { ai -= vp * rj[i]; aj -= vp * ri[i]; }
-                else if (t == i) { ai -= vp * rj[j]; aj -= vp * ri[j]; }
-                if (h == 0) gi0 += ai; else gi1 += ai;
-                if (j < i) Gp[(int64_t)P * N + t] = aj;
-            }
-            if ((tid & 31) == 0) gpart[2 * JK_G * JK_R - 1 - (tid >> 5)] = jown;   // 2 warps per row
-        }
-        // ---- scattered J_Q += v_PQ rho~_P for Q < P, thread-owned Q across the CTA's rows
-        {
-            int off[JK_R];
-            double rt[JK_R];
+                // ---- G_i partials stay per lane (reduced at slab end); G_j and J_P reduced now
 #pragma unroll
-            for (int r = 0; r < JK_R; ++r) {
-                const int j = min(j0 + r, i);
-                off[r] = (int)(rowbase(P0 + r, g) - rb0);
-                rt[r] = r < nr ? rho[i * N + j] * (i != j ? 2.0 : 1.0) : 0.0;
-            }
-            const int Pend = (int)(P0 + nr - 1);      // Q < P for some row of the chunk
-            const int Pfirst = (int)P0;
+                for (int u = 0; u < 4; ++u) gi[u] = fma(2.0, oJ[u], gi[u]);
+                for (int o = 1; o < S; o <<= 1)
 #pragma unroll
-            for (int q = 0; q < JK_NREG; ++q) {
-                const int Q = tid + q * JK_THREADS;
-                if (Q >= Pend) break;
-                double acc = 0.0;
-                if (Q < Pfirst) {                     // below every row of the chunk
+                    for (int u = 0; u < 4; ++u) oI[u] += shfl_x(oI[u], o);
 #pragma unroll
-                    for (int r = 0; r < JK_R; ++r)
-                        if (r < nr) acc += (double)cbuf[off[r] + Q] * rt[r];
-                } else {
+                for (int o = 1; o < 32; o <<= 1) jp += shfl_x(jp, o);
+                const double vp = (double)row[eri_ket(i, j)];
+                const double rjI = rho[rsw<NP>(j, i)], rjJ = rho[rsw<NP>(j, j)];
+                const double riI = rho[rsw<NP>(i, i)], riJ = rho[rsw<NP>(i, j)];
+                if (lane_ok && s == 0) {
+                    double *Gj = Gp + (tri(i) + j) * N;
 #pragma unroll
-                    for (int r = 0; r < JK_R; ++r)
-                        if (r < nr && Q < Pfirst + r) acc += (double)cbuf[off[r] + Q] * rt[r];
+                    for (int u = 0; u < 4; ++u) {
+                        const int t = 4 * a + u;
+                        double gJ = 2.0 * oI[u];
+                        if (t == j) { gi[u] -= vp * rjI; gJ -= vp * riI; }
+                        else if (t == i) { gi[u] -= vp * rjJ; gJ -= vp * riJ; }
+                        if (j < i && t <= i) Gj[t] = gJ;
+                    }
                 }
-                jsc[q] += acc;
+                if (lane == 0) Jp[tri(i) + j] = 2.0 * jp - vp * riJ * (i != j ? 2.0 : 1.0);
+            }
+            // ---- J_Q += v_PQ rho~_P over the chunk's rows, thread-owned 16-byte units
+            const int nr = min(CR, i + 1 - j0);
+            for (int rr = 0; rr < nr; ++rr) {
+                const int jj = j0 + rr;
+                const double wgt = rho[rsw<NP>(i, jj)] * (i != jj ? 2.0 : 1.0);
+                const ST *rowp = cbuf + (int64_t)rr * L;
+#pragma unroll
+                for (int k = 0; k < KU; ++k) {
+                    const int u = tid + k * JK_THREADS;
+                    const double wk = u < units ? wgt : 0.0;
+                    const int uc = min(u, units - 1);
+                    if constexpr (VW == 4) {
+                        const float4 v = reinterpret_cast<const float4 *>(rowp)[uc];
+                        acc[k][0] = fma((double)v.x, wk, acc[k][0]);
+                        acc[k][1] = fma((double)v.y, wk, acc[k][1]);
+                        acc[k][2] = fma((double)v.z, wk, acc[k][2]);
+                        acc[k][3] = fma((double)v.w, wk, acc[k][3]);
+                    } else {
+                        const double2 v = reinterpret_cast<const double2 *>(rowp)[uc];
+                        acc[k][0] = fma(v.x, wk, acc[k][0]);
+                        acc[k][1] = fma(v.y, wk, acc[k][1]);
+                    }
+                }
+            }
+            __syncthreads();                           // chunk consumed
+            if (tid == 0 && pi >= i0) issue(slot);
+        }
+        // ---- slab end: G_i = fixed-order sum over stride lanes, then over warps
+        for (int o = 1; o < S; o <<= 1)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) gi[u] += shfl_x(gi[u], o);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) gred[tid * 8 + u] = gi[u];
+        __syncthreads();
+        if (tid < A) {                                 // thread tid handles block tid
+            double *Gi = Gp + (tri(i) + i) * N;
+            for (int u = 0; u < 4; ++u) {
+                const int t = 4 * tid + u;
+                if (t > i) break;
+                double v = 0.0;
+                for (int ww = 0; ww < CR; ++ww) v += gred[(ww * 32 + tid * S) * 8 + u];
+                Gi[t] = v;
             }
         }
-        __syncthreads();                              // chunk consumed; J_P partials visible
-        if (tid < nr) {
-            const int w0 = 2 * JK_G * JK_R - 1 - 2 * tid;
-            Jp[P0 + tid] = gpart[w0] + gpart[w0 - 1];
-        }
-        if (tid == 0 && c + nbuf < nch) issue(c + nbuf);
-        if (j0 + nr == i + 1) {                       // slab complete: reduce G_i over the row groups
-            __syncthreads();
-            gpart[grp * 2 * JK_G + gt] = gi0;
-            gpart[grp * 2 * JK_G + JK_G + gt] = gi1;
-            __syncthreads();
-            if (tid <= i) {
-                double s = 0.0;
-                for (int r = 0; r < JK_R; ++r) s += gpart[r * 2 * JK_G + tid];
-                Gp[(tri(i) + i) * N + tid] = s;
-            }
-            gi0 = gi1 = 0.0;
-            __syncthreads();
-        }
+        __syncthreads();
     }
+    // ---- this CTA's J_Q partial, every Q of the molecule written once
     const int local = cta - b.m_jkcta0[m];
     double *Js = Jp + (int64_t)(1 + local) * npp;
+    const int64_t Lm = eri_rowlen(N - 1);
 #pragma unroll
-    for (int q = 0; q < JK_NREG; ++q) {
-        const int64_t e = tid + (int64_t)q * JK_THREADS;
-        if (e < npp) Js[e] = jsc[q];
-    }
+    for (int k = 0; k < KU; ++k)
+#pragma unroll
+        for (int v = 0; v < VW; ++v) {
+            const int e = (tid + k * JK_THREADS) * VW + v;
+            if (e >= Lm) continue;
+            const int tau = e >> 4;
+            int a = (int)((sqrt(8.0 * (double)tau + 1.0) - 1.0) * 0.5);
+            while (tri(a + 1) <= tau) ++a;
+            while (tri(a) > tau) --a;
+            const int bb = tau - (int)tri(a);
+            const int kk = 4 * a + ((e >> 2) & 3), ll = 4 * bb + (e & 3);
+            if (kk < N && ll <= kk) Js[tri(kk) + ll] = acc[k][v];
+        }
+}
+
+template <typename ST, int NB>
+static void launch_bucket(const DevBatch &b, const int *ctas, int n, cudaStream_t s) {
+    const size_t sm = JKPlan<ST, NB>::bytes;
+    cudaFuncSetAttribute(k_jk<ST, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_jk<ST, NB><<<n, JK_THREADS, sm, s>>>(b, ctas);
 }
 
 template <typename ST>
-static void launch_jk_t(const DevBatch &b, int nmax, cudaStream_t s) {
-    int nbuf = 2;
-    size_t sm = jk_layout<ST>(nmax, 2).total;
-    if (sm > 227 * 1024) {
-        nbuf = 1;
-        sm = jk_layout<ST>(nmax, 1).total;
-    }
-    cudaFuncSetAttribute(k_jk<ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_jk<ST><<<b.n_jk_cta, JK_THREADS, sm, s>>>(b, nbuf);
+static void launch_jk_t(const DevBatch &b, const int *bucket_ctas, const int *bucket_n, cudaStream_t s) {
+    const int *c = bucket_ctas;
+    if (bucket_n[0]) launch_bucket<ST, 16>(b, c, bucket_n[0], s);
+    c += bucket_n[0];
+    if (bucket_n[1]) launch_bucket<ST, 32>(b, c, bucket_n[1], s);
+    c += bucket_n[1];
+    if (bucket_n[2]) launch_bucket<ST, 48>(b, c, bucket_n[2], s);
+    c += bucket_n[2];
+    if (bucket_n[3]) launch_bucket<ST, 64>(b, c, bucket_n[3], s);
+    c += bucket_n[3];
+    if (bucket_n[4]) launch_bucket<ST, 80>(b, c, bucket_n[4], s);
+    c += bucket_n[4];
+    if (bucket_n[5]) launch_bucket<ST, 96>(b, c, bucket_n[5], s);
 }
 
-void launch_jk(const DevBatch &b, int nmax, cudaStream_t s) {
-    if (b.prec == 0) launch_jk_t<double>(b, nmax, s);
-    else launch_jk_t<float>(b, nmax, s);
+// bucket_ctas: device array of CTA indices grouped by AO-count bucket; bucket_n: host counts [6]
+int launch_jk(const DevBatch &b, const int *bucket_ctas, const int *bucket_n, cudaStream_t s) {
+    if (b.n_jk_cta == 0) return 0;
+    if (b.prec == 0) launch_jk_t<double>(b, bucket_ctas, bucket_n, s);
+    else launch_jk_t<float>(b, bucket_ctas, bucket_n, s);
+    int k = 0;
+    for (int i = 0; i < 6; ++i) k += bucket_n[i] > 0;
+    return k;
 }
 
 }  // namespace dftb

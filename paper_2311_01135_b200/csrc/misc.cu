@@ -80,12 +80,25 @@ __global__ void k_compact(DevBatch b, int mol, double eps, const double *qsp, in
                           double *ov) {
     __shared__ int64_t scan[128];
     const int64_t P = blockIdx.x;
-    const ST *row = (const ST *)b.eri + b.m_eri0[mol] + rowbase(P, 16 / (int)sizeof(ST));
+    int i = (int)((sqrt(8.0 * (double)P + 1.0) - 1.0) * 0.5);
+    while (tri(i + 1) <= P) ++i;
+    while (tri(i) > P) --i;
+    const int j = (int)(P - tri(i));
+    const ST *row = (const ST *)b.eri + b.m_eri0[mol] + eri_row(i, j);
     const double *qao = b.qao + b.m_npp0[mol];
     const int64_t len = P + 1, per = (len + 127) / 128;
     const int64_t lo = threadIdx.x * per, hi = min(len, lo + per);
+    auto ket = [&](int64_t q, int &k) {
+        k = (int)((sqrt(8.0 * (double)q + 1.0) - 1.0) * 0.5);
+        while (tri(k + 1) <= q) ++k;
+        while (tri(k) > q) --k;
+        return (double)row[eri_ket(k, (int)(q - tri(k)))];
+    };
     int64_t c = 0;
-    for (int64_t q = lo; q < hi; ++q) c += keep_entry((double)row[q], P, q, eps, qsp, qao);
+    for (int64_t q = lo; q < hi; ++q) {
+        int k;
+        c += keep_entry(ket(q, k), P, q, eps, qsp, qao);
+    }
     scan[threadIdx.x] = c;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -96,16 +109,10 @@ __global__ void k_compact(DevBatch b, int mol, double eps, const double *qsp, in
     __syncthreads();
     if (!rowoff) return;
     int64_t pos = rowoff[P] + scan[threadIdx.x];
-    int i = (int)((sqrt(8.0 * (double)P + 1.0) - 1.0) * 0.5);
-    while (tri(i + 1) <= P) ++i;
-    while (tri(i) > P) --i;
-    const int j = (int)(P - tri(i));
     for (int64_t q = lo; q < hi; ++q) {
-        const double v = (double)row[q];
+        int k;
+        const double v = ket(q, k);
         if (!keep_entry(v, P, q, eps, qsp, qao)) continue;
-        int k = (int)((sqrt(8.0 * (double)q + 1.0) - 1.0) * 0.5);
-        while (tri(k + 1) <= q) ++k;
-        while (tri(k) > q) --k;
         oi[pos] = (uint16_t)i; oj[pos] = (uint16_t)j;
         ok[pos] = (uint16_t)k; ol[pos] = (uint16_t)(q - tri(k));
         ov[pos] = v;

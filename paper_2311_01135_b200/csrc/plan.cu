@@ -23,7 +23,7 @@ void launch_eri(const DevBatch &b, const int64_t *tot, double eps, double prim_c
 void launch_enn(const DevBatch &b, cudaStream_t s);
 void launch_onee(const DevBatch &b, cudaStream_t s);
 void launch_grid(const DevBatch &b, int max_atoms, cudaStream_t s);
-void launch_jk(const DevBatch &b, int nmax, cudaStream_t s);
+int launch_jk(const DevBatch &b, const int *bucket_ctas, const int *bucket_n, cudaStream_t s);
 int launch_xc(const DevBatch &b, const int *bucket_ctas, const int *bucket_n, int nsh_max, cudaStream_t s);
 void launch_orth(const DevBatch &b, int nmax, cudaStream_t s);
 void launch_post(const DevBatch &b, int nmax, int it, int diis_start, int diis_hist, double damping,
@@ -53,6 +53,7 @@ static int fail(int code, const std::string &msg) {
     } while (0)
 
 static constexpr int XC_CHUNK = 2048;
+static constexpr int JK_SPLIT = 12;     // target J/K CTAs per molecule (largest slab permitting)
 
 struct dftb_plan {
     DevBatch d{};
@@ -62,10 +63,12 @@ struct dftb_plan {
     int nmax = 0, nsh_max = 0, natom_max = 0;
     int64_t cls_tot[NCLS] = {0}, pair_tot[3] = {0};
     std::vector<int> nao, nocc, jkc0, xcc0;
-    std::vector<int64_t> mat0, npp0, grid0;
+    std::vector<int64_t> mat0, npp0, grid0, eri0;
     int64_t launches = 0;
     int *xc_bucket_ctas = nullptr;  // device
     int xc_bucket_n[6] = {0};
+    int *jk_bucket_ctas = nullptr;  // device
+    int jk_bucket_n[6] = {0};
     bool timing = false;
     cudaEvent_t ev[8] = {nullptr};
     double stage_ms[8] = {0};
@@ -204,13 +207,32 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
         const int64_t N = p->nao[m], npp = N * (N + 1) / 2;
         p->mat0[m + 1] = p->mat0[m] + N * N;
         p->npp0[m + 1] = p->npp0[m] + npp;
-        eri0[m + 1] = eri0[m] + rowbase(npp, opts->precision ? 4 : 2);
+        eri0[m + 1] = eri0[m] + eri_size((int)N);
         G0[m + 1] = G0[m] + N * (N + 1) / 2 * N;
-        const int ncj = (int)((N + 1) / 2);
-        for (int c = 0; c < ncj; ++c) {
-            jk_mol.push_back(m);
-            jk_i0.push_back(c);
-            jk_i1.push_back((N - 1 - c) != c ? (int)(N - 1 - c) : -1);
+        // J/K CTAs: contiguous whole-slab ranges [i0, i1) of about equal tile-row work
+        // (slab i = the i + 1 store rows (i, j); its work is (i + 1) * tri(i/4 + 1) tiles)
+        int ncj = 0;
+        {
+            std::vector<int64_t> wk((size_t)N);
+            int64_t tot = 0, wmax = 0;
+            for (int i = 0; i < N; ++i) {
+                const int64_t A = i / 4 + 1;
+                wk[i] = (int64_t)(i + 1) * (A * (A + 1) / 2);
+                tot += wk[i];
+                wmax = std::max(wmax, wk[i]);
+            }
+            const int64_t target = std::max(wmax, (tot + JK_SPLIT - 1) / JK_SPLIT);
+            int hi = (int)N;
+            int64_t acc = 0;
+            for (int i = (int)N - 1; i >= 0; --i) {
+                if (acc > 0 && acc + wk[i] > target) {
+                    jk_mol.push_back(m); jk_i0.push_back(i + 1); jk_i1.push_back(hi); ++ncj;
+                    hi = i + 1;
+                    acc = 0;
+                }
+                acc += wk[i];
+            }
+            jk_mol.push_back(m); jk_i0.push_back(0); jk_i1.push_back(hi); ++ncj;
         }
         p->jkc0[m + 1] = p->jkc0[m] + ncj;
         Jp0[m + 1] = Jp0[m] + (int64_t)(ncj + 1) * npp;
@@ -235,6 +257,15 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
         p->xc_bucket_n[bkt] = (int)xc_sorted.size() - (bkt ? 0 : 0);
     }
     for (int bkt = 5; bkt > 0; --bkt) p->xc_bucket_n[bkt] -= p->xc_bucket_n[bkt - 1];
+    // J/K CTAs grouped the same way (one kernel instance per AO-count bucket)
+    std::vector<int> jk_sorted;
+    for (int bkt = 0; bkt < 6; ++bkt) {
+        const size_t before = jk_sorted.size();
+        for (int c = 0; c < (int)jk_mol.size(); ++c)
+            if ((p->nao[jk_mol[c]] + 15) / 16 - 1 == bkt) jk_sorted.push_back(c);
+        p->jk_bucket_n[bkt] = (int)(jk_sorted.size() - before);
+    }
+    p->eri0 = eri0;
     const int64_t npts_tot = a_grid0[in->n_atom];
     const int njk = (int)jk_mol.size(), nxc = (int)xc_mol.size();
     const int64_t mat = p->mat0[nm];
@@ -287,6 +318,7 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
     UP(jk_mol, int, jk_mol.data(), njk)
     UP(jk_i0, int, jk_i0.data(), njk)
     UP(jk_i1, int, jk_i1.data(), njk)
+    UP(jk_sorted, int, jk_sorted.data(), njk)
     UP(xc_mol, int, xc_mol.data(), nxc)
     UP(xc_p0, int64_t, xc_p0.data(), nxc)
     UP(xc_p1, int64_t, xc_p1.data(), nxc)
@@ -372,6 +404,7 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
     d.xc_mol = PTR(int, o_xc_mol); d.xc_p0 = PTR(int64_t, o_xc_p0); d.xc_p1 = PTR(int64_t, o_xc_p1);
     d.n_xc_cta = nxc;
     p->xc_bucket_ctas = PTR(int, o_xc_sorted);
+    p->jk_bucket_ctas = PTR(int, o_jk_sorted);
     d.g_xyz = PTR(double, o_gxyz); d.g_w = PTR(double, o_gw);
     double **mats[14] = {&d.S, &d.T, &d.V, &d.H, &d.X, &d.C, &d.Cp, &d.rho, &d.rho_prev, &d.F, &d.J, &d.K, &d.Vxc,
                          &d.scratch};
@@ -458,10 +491,10 @@ int dftb_plan_iterate(dftb_plan *p, int32_t it, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     const DevBatch &d = p->d;
     const dftb_opts &o = p->opts;
-    launch_jk(d, p->nmax, st);
+    const int njl = launch_jk(d, p->jk_bucket_ctas, p->jk_bucket_n, st);
     const int nxl = launch_xc(d, p->xc_bucket_ctas, p->xc_bucket_n, p->nsh_max, st);
     launch_post(d, p->nmax, it, o.diis_start, o.diis_history, o.damping_factor, o.convergence_std, st);
-    p->launches += 2 + nxl;
+    p->launches += 1 + njl + nxl;
     CK(cudaGetLastError());
     return 0;
 }
@@ -496,18 +529,14 @@ int dftb_plan_eri_load(dftb_plan *p, int32_t mol, int64_t count, const uint16_t 
     if (!p || mol < 0 || mol >= p->d.n_mol) return fail(DFTB_EINVAL, "bad arguments");
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t npp = p->npp0[mol + 1] - p->npp0[mol];
-    const int esz = p->d.prec ? 4 : 8, g = 16 / esz;
-    const int64_t n = rowbase(npp, g);
-    int64_t e0 = 0;
-    for (int m = 0; m < mol; ++m) e0 += rowbase(p->npp0[m + 1] - p->npp0[m], g);
+    const int esz = p->d.prec ? 4 : 8;
+    const int N = p->nao[mol];
+    const int64_t n = eri_size(N);
+    const int64_t e0 = p->eri0[mol];
     std::vector<unsigned char> host((size_t)n * esz, 0);
     for (int64_t e = 0; e < count; ++e) {
-        int64_t P = (int64_t)i[e] * (i[e] + 1) / 2 + j[e], Q = (int64_t)k[e] * (k[e] + 1) / 2 + l[e];
-        if (i[e] < j[e]) P = (int64_t)j[e] * (j[e] + 1) / 2 + i[e];
-        if (k[e] < l[e]) Q = (int64_t)l[e] * (l[e] + 1) / 2 + k[e];
-        if (P < Q) std::swap(P, Q);
-        if (P >= npp) return fail(DFTB_EINVAL, "index out of range for n_ao");
-        const int64_t off = rowbase(P, g) + Q;
+        if (i[e] >= N || j[e] >= N || k[e] >= N || l[e] >= N) return fail(DFTB_EINVAL, "index out of range for n_ao");
+        const int64_t off = eri_pos(i[e], j[e], k[e], l[e]);
         if (esz == 8) reinterpret_cast<double *>(host.data())[off] = v[e];
         else reinterpret_cast<float *>(host.data())[off] = (float)v[e];
     }
@@ -630,7 +659,7 @@ int dftb_plan_jk(dftb_plan *p, const double *rho_host, double *J_host, double *K
     cudaStream_t st = (cudaStream_t)stream;
     int rc = upload_rho(p, rho_host, st);
     if (rc) return rc;
-    launch_jk(p->d, p->nmax, st);
+    launch_jk(p->d, p->jk_bucket_ctas, p->jk_bucket_n, st);
     launch_reduce(p->d, 1, st);
     CK(cudaGetLastError());
     const size_t nb = sizeof(double) * p->mat0[p->d.n_mol];
@@ -766,21 +795,23 @@ int dftb_plan_get(dftb_plan *p, const char *which, int32_t mol, double *host, in
     else if (w == "eri") {
         // returned unpadded, in canonical composite order (row P, Q <= P)
         const int64_t npp = p->npp0[mol + 1] - p->npp0[mol];
-        const int esz = d.prec ? 4 : 8, g = 16 / esz;
+        const int esz = d.prec ? 4 : 8;
+        const int N = p->nao[mol];
         cnt = npp * (npp + 1) / 2;
         if (n < cnt) return fail(DFTB_EINVAL, "host buffer too small");
-        int64_t e0 = 0;
-        for (int m = 0; m < mol; ++m) e0 += rowbase(p->npp0[m + 1] - p->npp0[m], g);
-        const int64_t padded = rowbase(npp, g);
-        std::vector<unsigned char> tmp((size_t)padded * esz);
-        CK(cudaMemcpyAsync(tmp.data(), (unsigned char *)d.eri + (size_t)e0 * esz, tmp.size(), cudaMemcpyDeviceToHost, st));
+        std::vector<unsigned char> tmp((size_t)eri_size(N) * esz);
+        CK(cudaMemcpyAsync(tmp.data(), (unsigned char *)d.eri + (size_t)p->eri0[mol] * esz, tmp.size(),
+                           cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        for (int64_t P = 0; P < npp; ++P)
-            for (int64_t Q = 0; Q <= P; ++Q) {
-                const int64_t src = rowbase(P, g) + Q;
-                host[P * (P + 1) / 2 + Q] = esz == 8 ? reinterpret_cast<double *>(tmp.data())[src]
-                                                     : (double)reinterpret_cast<float *>(tmp.data())[src];
-            }
+        int64_t o = 0;
+        for (int ii = 0; ii < N; ++ii)
+            for (int jj = 0; jj <= ii; ++jj)
+                for (int kk = 0; kk <= ii; ++kk)
+                    for (int ll = 0; ll <= (kk == ii ? jj : kk); ++ll, ++o) {
+                        const int64_t src = eri_row(ii, jj) + eri_ket(kk, ll);
+                        host[o] = esz == 8 ? reinterpret_cast<double *>(tmp.data())[src]
+                                           : (double)reinterpret_cast<float *>(tmp.data())[src];
+                    }
         return 0;
     } else {
         return fail(DFTB_EINVAL, "unknown buffer " + w);
