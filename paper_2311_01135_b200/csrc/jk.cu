@@ -33,6 +33,9 @@
 namespace dftb {
 
 
+#ifndef JK_NBUF_MAX
+#define JK_NBUF_MAX 2                          // staging buffers per CTA
+#endif
 constexpr int JK_WARPS = 4;                    // one store row per warp
 constexpr int JK_THREADS = 32 * JK_WARPS;
 
@@ -94,9 +97,9 @@ struct JKPlan {
     static constexpr int AMAX = NB / 4;
     static constexpr int LMAX = 8 * AMAX * (AMAX + 1);
     static constexpr size_t row_bytes = (size_t)LMAX * sizeof(ST);
-    static constexpr size_t fixed = 128 + sizeof(double) * ((size_t)NB * NB + 8 * JK_THREADS);
+    static constexpr size_t fixed = 128 + sizeof(double) * ((size_t)NB * NB + 4 * JK_THREADS);
     static constexpr size_t cap = 227 * 1024;
-    static constexpr int NBUF = fixed + 2 * JK_WARPS * row_bytes <= cap ? 2 : 1;
+    static constexpr int NBUF = JK_NBUF_MAX > 1 && fixed + 2 * JK_WARPS * row_bytes <= cap ? 2 : 1;
     static constexpr int CR = fixed + NBUF * JK_WARPS * row_bytes <= cap ? JK_WARPS : JK_WARPS / 2;
     static constexpr size_t bytes = fixed + NBUF * CR * row_bytes;
     static_assert(bytes <= 227 * 1024, "J/K bucket does not fit in shared memory");
@@ -110,12 +113,16 @@ __device__ __forceinline__ int rsw(int r, int c) {
     static_assert(NP % 16 == 0, "chunk swizzle needs NP / 2 to be a multiple of 8");
     return r * NP + (((c >> 1) ^ ((r >> 2) & 7)) << 1) + (c & 1);
 }
-template <int NP>
-__device__ __forceinline__ void ld4r(const double *rho, int r, int c4, double (&v)[4]) {   // c4 % 4 == 0
-    const double2 a = *reinterpret_cast<const double2 *>(rho + rsw<NP>(r, c4));
-    const double2 c = *reinterpret_cast<const double2 *>(rho + rsw<NP>(r, c4 + 2));
+
+// 4 consecutive rho values of a swizzled row starting at column 2*c2 (c2 = 16-byte chunk
+// index, even); key = that row's swizzle key ((r >> 2) & 7)
+__device__ __forceinline__ void ld4k(const double *rowp, int c2, int key, double (&v)[4]) {
+    const int k0 = c2 ^ key;
+    const double2 a = *reinterpret_cast<const double2 *>(rowp + 2 * k0);
+    const double2 c = *reinterpret_cast<const double2 *>(rowp + 2 * (k0 ^ 1));
     v[0] = a.x; v[1] = a.y; v[2] = c.x; v[3] = c.y;
 }
+__device__ __forceinline__ int tri32(int a) { return (a * (a + 1)) >> 1; }
 
 // NB: AO-count bound of the bucket (multiple of 16) — fixes the padded rho stride, the
 // staging size and the number of J_Q units each thread owns.
@@ -129,8 +136,8 @@ __global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, const int *ctas) 
     extern __shared__ __align__(128) unsigned char jsm[];
     uint64_t *bar = (uint64_t *)jsm;
     double *rho = (double *)(jsm + 128);                        // [NP][NP] swizzled, zero padded
-    double *gred = rho + NP * NP;                               // [JK_THREADS][8]
-    ST *stage = (ST *)(gred + 8 * JK_THREADS);                  // [NBUF][CR * LMAX]
+    double *gred = rho + NP * NP;                               // [JK_THREADS][4]
+    ST *stage = (ST *)(gred + 4 * JK_THREADS);                  // [NBUF][CR * LMAX]
     const int cta = ctas[blockIdx.x];
     const int m = b.jk_mol[cta];
     if (b.done[m]) return;
@@ -175,6 +182,8 @@ __global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, const int *ctas) 
         const int S = A <= 1 ? 32 : A <= 2 ? 16 : A <= 4 ? 8 : A <= 8 ? 4 : A <= 16 ? 2 : 1;
         const int a = lane / S, s = lane % S;
         const bool lane_ok = a < A;
+        const int key_a = a & 7, key_i = (i >> 2) & 7;
+        const double *rhoA = rho + 4 * a * NP, *rhoI = rho + i * NP;
         const int64_t L = eri_rowlen(i);
         const int units = (int)(L / VW);
         double gi[4] = {0, 0, 0, 0};
@@ -185,6 +194,8 @@ __global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, const int *ctas) 
             const int j = j0 + w;
             if (w < CR && j <= i) {                    // warp-uniform
                 const ST *row = cbuf + (int64_t)w * L;
+                const double *rhoJ = rho + j * NP;
+                const int key_j = (j >> 2) & 7;
                 double oI[4] = {0, 0, 0, 0}, oJ[4] = {0, 0, 0, 0}, jp = 0.0;
                 if (lane_ok) {
                     // block a: row part tiles (a, q), q = 0..a, then column part tiles
@@ -193,15 +204,17 @@ __global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, const int *ctas) 
                         const bool rp = q <= a;
                         const int ta = rp ? a : q - 1, tb = rp ? q : a;   // tile (ta, tb)
                         const int beta = rp ? q : q - 1;                  // rho block of the product
+                        const bool dg = ta == tb;
                         float tf[16];
                         {
-                            const float4 *qp = reinterpret_cast<const float4 *>(row + 16 * (tri(ta) + tb));
+                            const float4 *qp = reinterpret_cast<const float4 *>(row + 16 * (tri32(ta) + tb));
                             if constexpr (sizeof(ST) == 4) {
 #pragma unroll
                                 for (int r = 0; r < 4; ++r) {
                                     const float4 v = qp[r];
                                     tf[4 * r] = v.x; tf[4 * r + 1] = v.y; tf[4 * r + 2] = v.z; tf[4 * r + 3] = v.w;
                                 }
+                                if (dg) { tf[0] *= 0.5f; tf[5] *= 0.5f; tf[10] *= 0.5f; tf[15] *= 0.5f; }
                             }
                         }
                         double t[16];
@@ -213,7 +226,7 @@ __global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, const int *ctas) 
                                     t[4 * r + c] = (double)(rp ? tf[4 * r + c] : tf[4 * c + r]);
                         } else {
                             double td[16];
-                            const double2 *qp = reinterpret_cast<const double2 *>(row + 16 * (tri(ta) + tb));
+                            const double2 *qp = reinterpret_cast<const double2 *>(row + 16 * (tri32(ta) + tb));
 #pragma unroll
                             for (int r = 0; r < 8; ++r) {
                                 const double2 v = qp[r];
@@ -223,16 +236,16 @@ __global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, const int *ctas) 
                             for (int r = 0; r < 4; ++r)
 #pragma unroll
                                 for (int c = 0; c < 4; ++c) t[4 * r + c] = rp ? td[4 * r + c] : td[4 * c + r];
+                            if (dg) { t[0] *= 0.5; t[5] *= 0.5; t[10] *= 0.5; t[15] *= 0.5; }
                         }
-                        if (ta == tb) { t[0] *= 0.5; t[5] *= 0.5; t[10] *= 0.5; t[15] *= 0.5; }
                         double jv[4], iv[4];
-                        ld4r<NP>(rho, j, 4 * beta, jv);
-                        ld4r<NP>(rho, i, 4 * beta, iv);
+                        ld4k(rhoJ, 2 * beta, key_j, jv);
+                        ld4k(rhoI, 2 * beta, key_i, iv);
                         const double jw = rp ? 1.0 : 0.0;      // J_P: row-part tiles only
 #pragma unroll
                         for (int rr = 0; rr < 4; ++rr) {
                             double x[4];
-                            ld4r<NP>(rho, 4 * a + rr, 4 * beta, x);
+                            ld4k(rhoA + rr * NP, 2 * beta, key_a, x);
                             double d = 0.0;
 #pragma unroll
                             for (int cc = 0; cc < 4; ++cc) {
@@ -300,7 +313,7 @@ __global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, const int *ctas) 
 #pragma unroll
             for (int u = 0; u < 4; ++u) gi[u] += shfl_x(gi[u], o);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) gred[tid * 8 + u] = gi[u];
+        for (int u = 0; u < 4; ++u) gred[tid * 4 + u] = gi[u];
         __syncthreads();
         if (tid < A) {                                 // thread tid handles block tid
             double *Gi = Gp + (tri(i) + i) * N;
@@ -308,7 +321,7 @@ __global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, const int *ctas) 
                 const int t = 4 * tid + u;
                 if (t > i) break;
                 double v = 0.0;
-                for (int ww = 0; ww < CR; ++ww) v += gred[(ww * 32 + tid * S) * 8 + u];
+                for (int ww = 0; ww < CR; ++ww) v += gred[(ww * 32 + tid * S) * 4 + u];
                 Gi[t] = v;
             }
         }

@@ -74,6 +74,8 @@ struct dftb_plan {
     double stage_ms[8] = {0};
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t aux = nullptr;     // J/K runs here, concurrently with XC on the caller's stream
+    cudaEvent_t fork = nullptr, join = nullptr;
 };
 
 // ------------------------------------------------------------------ Boys table (per device)
@@ -116,9 +118,13 @@ int dftb_device_count(int *count) {
 
 int dftb_plan_destroy(dftb_plan *p) {
     if (!p) return 0;
+    if (p->aux) cudaStreamSynchronize(p->aux);
     if (p->mem) cudaFreeAsync(p->mem, p->stream);   // back to the retained stream-ordered pool
     for (auto &e : p->ev)
         if (e) cudaEventDestroy(e);
+    if (p->fork) cudaEventDestroy(p->fork);
+    if (p->join) cudaEventDestroy(p->join);
+    if (p->aux) cudaStreamDestroy(p->aux);
     delete p;
     return 0;
 }
@@ -366,9 +372,16 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
         pool_set[p->device] = true;
     }
     p->stream = st;
+    if (cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->join, cudaEventDisableTiming) != cudaSuccess) {
+        dftb_plan_destroy(p);
+        return fail(DFTB_ECUDA, "stream/event creation failed");
+    }
     cudaError_t ce = cudaMallocAsync((void **)&p->mem, p->mem_bytes, st);
     if (ce != cudaSuccess) {
-        delete p;
+        p->mem = nullptr;
+        dftb_plan_destroy(p);
         return fail(DFTB_ERESOURCE, std::string("device allocation of ") + std::to_string(p->mem_bytes >> 20) +
                                         " MiB failed: " + cudaGetErrorString(ce));
     }
@@ -491,8 +504,14 @@ int dftb_plan_iterate(dftb_plan *p, int32_t it, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     const DevBatch &d = p->d;
     const dftb_opts &o = p->opts;
-    const int njl = launch_jk(d, p->jk_bucket_ctas, p->jk_bucket_n, st);
+    // J/K (aux stream) and XC (caller's stream) both read rho and write separate partials:
+    // fork/join so their CTAs share the SMs (FP64/XU-heavy vs FP32-heavy, smem fits both)
+    CK(cudaEventRecord(p->fork, st));
+    CK(cudaStreamWaitEvent(p->aux, p->fork, 0));
+    const int njl = launch_jk(d, p->jk_bucket_ctas, p->jk_bucket_n, p->aux);
     const int nxl = launch_xc(d, p->xc_bucket_ctas, p->xc_bucket_n, p->nsh_max, st);
+    CK(cudaEventRecord(p->join, p->aux));
+    CK(cudaStreamWaitEvent(st, p->join, 0));
     launch_post(d, p->nmax, it, o.diis_start, o.diis_history, o.damping_factor, o.convergence_std, st);
     p->launches += 1 + njl + nxl;
     CK(cudaGetLastError());
