@@ -16,6 +16,8 @@ from .errors import DeskDFTError, DeviceError, DimensionError, ResourceLimitErro
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libqm1b_b200.so")
+# development override (A/B timing of two builds in one process tree); never set in production
+LIB_PATH = os.environ.get("QM1B_B200_LIB", LIB_PATH)
 NMAX = 96
 
 c_i32p = ctypes.POINTER(ctypes.c_int32)
