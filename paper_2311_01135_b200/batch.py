@@ -199,3 +199,34 @@ def check_basis_supported(basis: BasisSet, zs) -> None:
             fused_element(basis, z)
         except BasisError:
             raise
+
+
+def check(mols: list[Molecule], basis: BasisSet, max_n_ao: int = 128) -> list:
+    """Per-molecule validation with pack()'s rules and error classes: returns, for each
+    molecule, None or the exception pack() would raise for it alone.  Lets a caller drop
+    bad entries from a batch instead of failing the whole batch (pipeline.run)."""
+    tab = _table(basis)
+    out = []
+    for m in mols:
+        try:
+            zs = np.asarray(m.atomic_numbers, np.int64)
+            if zs.max() > tab.zmax or not tab.ok[zs].all():
+                bad = sorted({int(z) for z in zs if z > tab.zmax or not tab.ok[z]})
+                missing = [z for z in bad if z not in basis.shells]
+                if missing:
+                    raise BasisError(f"basis {basis.name!r} missing element(s) Z={missing}")
+                fused_element(basis, bad[0])
+            nelec = int(zs.sum()) - int(m.charge)
+            if nelec <= 0 or nelec % 2:
+                raise MoleculeError(f"electron count {nelec}: restricted-closed-shell violation")
+            nao = int(tab.nao[zs].sum())
+            if nelec // 2 > nao:
+                raise MoleculeError(f"{nelec} electrons need {nelec // 2} orbitals but basis has {nao}")
+            if nao > max_n_ao:
+                raise ResourceLimitError(f"N={nao} exceeds configured maximum {max_n_ao}")
+            if nao > NMAX:
+                raise ResourceLimitError(f"N={nao} exceeds the device path maximum {NMAX}")
+            out.append(None)
+        except (BasisError, MoleculeError, ResourceLimitError) as exc:
+            out.append(exc)
+    return out

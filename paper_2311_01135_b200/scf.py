@@ -95,15 +95,17 @@ def _result(res, m: int, nocc: int, n_ao: int, dtype) -> SCFResult:
 
 
 def scf_batch(mols: list[Molecule], b: BasisSet, opts: SCFOptions | None = None,
-              errors: str = "raise") -> list:
+              errors: str = "raise", stream=None) -> list:
     """Run the SCF for every molecule of `mols` in one device batch.
 
     errors="raise" raises the first per-molecule failure (the reference's exception
-    class); errors="return" puts the exception object in that molecule's slot."""
+    class); errors="return" puts the exception object in that molecule's slot.
+    `stream`: CUDA stream handle (int / c_void_p) to run on; default the current torch
+    stream.  The call returns when the batch's results are on the host."""
     opts = opts or SCFOptions()
     if not mols:
         return []
-    with Plan(list(mols), b, opts.engine()) as plan:
+    with Plan(list(mols), b, opts.engine(), stream=stream) as plan:
         plan.run()
         res = plan.fetch()
     out = []

@@ -57,3 +57,52 @@ try:
         print("E sample", res.E_total[:4], "status", np.unique(res.status))
 except Exception:
     traceback.print_exc()
+
+try:
+    section("pipelined: plans in flight on separate streams, 256 x 9 heavy f32, 12 steps")
+    import torch
+    opts = SCFOptions(max_iterations=20, convergence_std=0.0, grid_level=0, precision="f32")
+    nmax_fl = int(os.environ.get("MAX_INFLIGHT", "4"))
+    streams = [torch.cuda.Stream() for _ in range(nmax_fl)]
+    plans = [Plan(synth.batch(256, 9, seed=1 + k), b, opts.engine(), stream=s.cuda_stream)
+             for k, s in enumerate(streams)]
+    for p in plans:
+        p.run()
+    torch.cuda.synchronize()
+    for nfl in range(1, nmax_fl + 1):
+        K = 12
+        t = time.time()
+        for k in range(K):
+            plans[k % nfl].run()
+        torch.cuda.synchronize()
+        dt = time.time() - t
+        print("in_flight", nfl, "wall %.3f s" % dt, "mol/s %.1f" % (256 * K / dt))
+    # staggered: batch k+1's setup/ERI waits for batch k's setup/ERI, so it overlaps k's SCF loop
+    for nfl in range(2, nmax_fl + 1):
+        K = 12
+        evs = [torch.cuda.Event() for _ in range(nfl)]
+        t = time.time()
+        for k in range(K):
+            s_k, p = streams[k % nfl], plans[k % nfl]
+            if k > 0:
+                s_k.wait_event(evs[(k - 1) % nfl])
+            p.begin()
+            evs[k % nfl].record(s_k)
+            for it in range(20):
+                p.iterate(it)
+        torch.cuda.synchronize()
+        dt = time.time() - t
+        print("staggered in_flight", nfl, "wall %.3f s" % dt, "mol/s %.1f" % (256 * K / dt))
+    for p in plans:
+        p.close()
+    big = Plan(synth.batch(512, 9, seed=11), b, opts.engine())
+    big.run(); torch.cuda.synchronize()
+    t = time.time()
+    for k in range(4):
+        big.run()
+    torch.cuda.synchronize()
+    dt = time.time() - t
+    print("single plan 512 mols", "mol/s %.1f" % (512 * 4 / dt))
+    big.close()
+except Exception:
+    traceback.print_exc()
