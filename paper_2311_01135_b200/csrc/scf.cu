@@ -15,6 +15,7 @@ namespace dftb {
 
 constexpr int SCF_THREADS = 256;
 constexpr int KP = 32;  // GEMM K-panel
+constexpr int GST = (KP * NMAX + 255) / 256;   // staging elements per thread per operand (256 threads)
 
 struct Arena {
     int nm;             // arena dimension (largest N of the batch) and staging leading dim
@@ -33,7 +34,7 @@ struct Arena {
 
 constexpr int NPH = NMAX / 2 + 1;
 
-HD size_t arena_w(int nm) { return (size_t)(nm * nm > 2 * KP * nm ? nm * nm : 2 * KP * nm); }
+HD size_t arena_w(int nm) { return (size_t)(nm * nm > 2 * KP * 64 ? nm * nm : 2 * KP * 64); }
 
 __device__ __forceinline__ Arena carve(unsigned char *base, int nm) {
     Arena a;
@@ -43,7 +44,7 @@ __device__ __forceinline__ Arena carve(unsigned char *base, int nm) {
     a.B = p; p += nm * nm;
     a.W = p; p += arena_w(nm);
     a.sa = a.W;
-    a.sb = a.W + KP * nm;
+    a.sb = a.W + KP * 64;
     a.cs = p; p += 2 * NPH;
     a.sn = p; p += 2 * NPH;
     a.dv = p; p += NMAX;
@@ -65,57 +66,83 @@ size_t scf_smem_bytes(int nm) {
 }
 
 // C (M x N, ldc) = alpha * op(A) op(B) + beta * C ; op(A) is M x K, op(B) is K x N.
-// Operands may live in global or shared memory; M, N <= NMAX.
+// Operands may live in global or shared memory; M, N <= NMAX.  The output is computed in
+// 64 x 64 blocks (one for M, N <= 64): 16 x 16 threads with 4 x 4 register tiles, K in
+// panels of KP staged zero-padded into ar.sa / ar.sb ([KP][64] each), so the inner loop has
+// no bounds tests.  C must not alias A or B (blocks are written as they finish).
 __device__ void cta_gemm(double *C, int ldc, const double *A, int lda, bool tA, const double *B, int ldb,
                          bool tB, int M, int N, int K, double alpha, double beta, const Arena &ar) {
-    const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;  // 16 x 16 threads, 6 x 6 tiles
-    const int LD = ar.nm;
-    double acc[6][6];
+    const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+    double *const sa = ar.sa, *const sb = ar.sb;
+    constexpr int SU = KP * 64 / SCF_THREADS;           // staged elements per thread per operand
+    for (int i0 = 0; i0 < M; i0 += 64)
+        for (int j0 = 0; j0 < N; j0 += 64) {
+            double acc[4][4];
 #pragma unroll
-    for (int a = 0; a < 6; ++a)
+            for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int c = 0; c < 6; ++c) acc[a][c] = 0.0;
-    for (int k0 = 0; k0 < K; k0 += KP) {
-        const int kn = min(KP, K - k0);
-        // staging loops map consecutive threads to the operand's contiguous index (coalesced)
-        for (int t = tid; t < KP * LD; t += SCF_THREADS) {
-            int kk, i;
-            if (tA) { kk = t / LD; i = t - kk * LD; } else { i = t / KP; kk = t - i * KP; }
-            double va = 0.0;
-            if (kk < kn && i < M) va = tA ? A[(int64_t)(k0 + kk) * lda + i] : A[(int64_t)i * lda + k0 + kk];
-            ar.sa[kk * LD + i] = va;
-        }
-        for (int t = tid; t < KP * LD; t += SCF_THREADS) {
-            int kk, j;
-            if (!tB) { kk = t / LD; j = t - kk * LD; } else { j = t / KP; kk = t - j * KP; }
-            double vb = 0.0;
-            if (kk < kn && j < N) vb = tB ? B[(int64_t)j * ldb + k0 + kk] : B[(int64_t)(k0 + kk) * ldb + j];
-            ar.sb[kk * LD + j] = vb;
-        }
-        __syncthreads();
-        for (int kk = 0; kk < kn; ++kk) {
-            double av[6], bv[6];
+                for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+            for (int k0 = 0; k0 < K; k0 += KP) {
+                const int kn = min(KP, K - k0);
+                double v[SU];
 #pragma unroll
-            for (int a = 0; a < 6; ++a) av[a] = (ty + 16 * a < LD) ? ar.sa[kk * LD + ty + 16 * a] : 0.0;
+                for (int u = 0; u < SU; ++u) {
+                    const int t = tid + u * SCF_THREADS;
+                    int kk, i;
+                    if (tA) { kk = t >> 6; i = t & 63; } else { i = t / KP; kk = t - i * KP; }
+                    const int gi = i0 + i;
+                    v[u] = (kk < kn && gi < M) ? (tA ? A[(int64_t)(k0 + kk) * lda + gi]
+                                                     : A[(int64_t)gi * lda + k0 + kk]) : 0.0;
+                }
 #pragma unroll
-            for (int c = 0; c < 6; ++c) bv[c] = (tx + 16 * c < LD) ? ar.sb[kk * LD + tx + 16 * c] : 0.0;
+                for (int u = 0; u < SU; ++u) {
+                    const int t = tid + u * SCF_THREADS;
+                    int kk, i;
+                    if (tA) { kk = t >> 6; i = t & 63; } else { i = t / KP; kk = t - i * KP; }
+                    sa[kk * 64 + i] = v[u];
+                }
 #pragma unroll
-            for (int a = 0; a < 6; ++a)
+                for (int u = 0; u < SU; ++u) {
+                    const int t = tid + u * SCF_THREADS;
+                    int kk, j;
+                    if (!tB) { kk = t >> 6; j = t & 63; } else { j = t / KP; kk = t - j * KP; }
+                    const int gj = j0 + j;
+                    v[u] = (kk < kn && gj < N) ? (tB ? B[(int64_t)gj * ldb + k0 + kk]
+                                                     : B[(int64_t)(k0 + kk) * ldb + gj]) : 0.0;
+                }
 #pragma unroll
-                for (int c = 0; c < 6; ++c) acc[a][c] = fma(av[a], bv[c], acc[a][c]);
-        }
-        __syncthreads();
-    }
+                for (int u = 0; u < SU; ++u) {
+                    const int t = tid + u * SCF_THREADS;
+                    int kk, j;
+                    if (!tB) { kk = t >> 6; j = t & 63; } else { j = t / KP; kk = t - j * KP; }
+                    sb[kk * 64 + j] = v[u];
+                }
+                __syncthreads();
+#pragma unroll 4
+                for (int kk = 0; kk < kn; ++kk) {
+                    double av[4], bv[4];
 #pragma unroll
-    for (int a = 0; a < 6; ++a)
+                    for (int a = 0; a < 4; ++a) av[a] = sa[kk * 64 + ty + 16 * a];
 #pragma unroll
-        for (int c = 0; c < 6; ++c) {
-            const int i = ty + 16 * a, j = tx + 16 * c;
-            if (i < M && j < N) {
-                double v = alpha * acc[a][c];
-                if (beta != 0.0) v += beta * C[(int64_t)i * ldc + j];
-                C[(int64_t)i * ldc + j] = v;
+                    for (int c = 0; c < 4; ++c) bv[c] = sb[kk * 64 + tx + 16 * c];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) acc[a][c] = fma(av[a], bv[c], acc[a][c]);
+                }
+                __syncthreads();
             }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int i = i0 + ty + 16 * a, j = j0 + tx + 16 * c;
+                    if (i < M && j < N) {
+                        double x = alpha * acc[a][c];
+                        if (beta != 0.0) x += beta * C[(int64_t)i * ldc + j];
+                        C[(int64_t)i * ldc + j] = x;
+                    }
+                }
         }
     __syncthreads();
 }
@@ -146,7 +173,7 @@ __device__ __forceinline__ void jac_angle(double app, double aqq, double apq, do
 }
 
 __device__ double *cta_jacobi(double *A0, double *A1, double *V, int n, const Arena &ar, int *nsweeps,
-                              int max_sweeps = 30) {
+                              int max_sweeps = 30, double tol = 1e-13) {
     const int tid = threadIdx.x, nt = SCF_THREADS;
     const int n2 = n + (n & 1), np = n2 / 2, R = n2 - 1;
     const int nblk = np * np, ntask = nblk + n * np;
@@ -187,7 +214,7 @@ __device__ double *cta_jacobi(double *A0, double *A1, double *V, int n, const Ar
             }
             off = block_max(off, ar.red);
             dg = block_max(dg, ar.red);
-            if (off <= 1e-13 * dg || off < 1e-300 || sweeps >= max_sweeps) break;
+            if (off <= tol * dg || off < 1e-300 || sweeps >= max_sweeps) break;
             ++sweeps;
         }
         const double *cs = ar.cs + bf * NPH, *sn = ar.sn + bf * NPH;
@@ -255,9 +282,15 @@ __device__ double *cta_jacobi(double *A0, double *A1, double *V, int n, const Ar
 }
 
 // ascending order of diag(A) -> ar.perm (rank of each original index), stable by index
+__device__ void sort_dv(int n, const Arena &ar);
 __device__ void sort_eigs(const double *A, int n, const Arena &ar) {
     for (int i = threadIdx.x; i < n; i += SCF_THREADS) ar.dv[i] = A[i * n + i];
     __syncthreads();
+    sort_dv(n, ar);
+}
+
+// ar.perm = ascending rank of ar.dv (ties by index)
+__device__ void sort_dv(int n, const Arena &ar) {
     for (int i = threadIdx.x; i < n; i += SCF_THREADS) {
         const double d = ar.dv[i];
         int r = 0;
@@ -567,7 +600,9 @@ __global__ void __launch_bounds__(SCF_THREADS, 2) k_post(DevBatch b, PostArgs pa
     // (9) Roothaan: F' = X^T F X, Jacobi (warm start from previous C'), C = X C'
     cta_gemm(S2, N, Fuse, N, false, X, N, false, N, M, N, 1.0, 0.0, ar);     // F X  (N x M, ld N)
     cta_gemm(ar.A, M, X, N, true, S2, N, false, M, M, N, 1.0, 0.0, ar);      // X^T (F X)
+    const double *Ad = nullptr;
     if (it >= 0) {
+        // warm start: Jacobi on C'^T F' C' with V = C' (previous eigenvectors)
         cta_gemm(S1, M, ar.A, M, false, Cp, M, false, M, M, M, 1.0, 0.0, ar); // F' C'
         cta_gemm(ar.A, M, Cp, M, true, S1, M, false, M, M, M, 1.0, 0.0, ar);  // C'^T F' C'
         for (int t = tid; t < M * M; t += SCF_THREADS) ar.B[t] = Cp[t];
@@ -575,12 +610,14 @@ __global__ void __launch_bounds__(SCF_THREADS, 2) k_post(DevBatch b, PostArgs pa
         for (int t = tid; t < M * M; t += SCF_THREADS) ar.B[t] = (t / M == t % M) ? 1.0 : 0.0;
     }
     __syncthreads();
+    {
+        int nsw = 0;
+        Ad = cta_jacobi(ar.A, ar.W, ar.B, M, ar, &nsw);
+        if (dbg && tid == 0) dbg[10] += nsw;
+    }
     tick(4);
-    int nsw = 0;
-    const double *Ad = cta_jacobi(ar.A, ar.W, ar.B, M, ar, &nsw);
-    if (dbg && tid == 0) dbg[10] += nsw;
-    tick(5);
     sort_eigs(Ad, M, ar);
+    tick(5);
     for (int t = tid; t < M * M; t += SCF_THREADS) {
         const int row = t / M, i = t % M;
         Cp[row * M + ar.perm[i]] = ar.B[t];
