@@ -227,6 +227,17 @@ def run_reference(args, ws, rank):
 
 
 # ----------------------------------------------------------------------------- GPU arm
+def _eri_traffic():
+    """DRAM bytes (read + write) of one step's ERI stage from the committed ncu --set full
+    capture (profiles/r1_eri_traffic.json), or None when the summary is absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_eri_traffic.json")) as fh:
+            d = json.load(fh)
+        return d["eri_stage_dram_read_bytes"] + d["eri_stage_dram_write_bytes"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def run_ours(args, ws, rank, local):
     import torch
 
@@ -359,7 +370,7 @@ def run_ours(args, ws, rank, local):
         "roofline": {"kernel": "ERI stage (k_pairs, k_schwarz, 6 x k_eri)", "bound": "fp64",
                      "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
                      "frac": achieved / peak.value if peak.value else None,
-                     "traffic": None,
+                     "traffic": _eri_traffic(),
                      "algorithmic": "SURVEY 8(d): 81 x F(class) per split-shell quartet surviving "
                                     f"Schwarz {opts.screen_eps:g}; {nq} quartets, {flops / 1e12:.3f} TFLOP per step",
                      "peak_source": "measured: dftb_fma_peak FP64 FMA probe on this GPU "

@@ -111,7 +111,9 @@ __device__ __forceinline__ void load_geo(const DevBatch &b, int64_t pr, double *
 
 template <typename ST>
 __device__ __forceinline__ void store_eri(ST *eri, int64_t base, int i, int j, int k, int l, double v) {
-    eri[base + eri_pos(i, j, k, l)] = (ST)v;
+    // written once, read by the next stage: streaming (evict-first) store, so the output
+    // does not push the primitive-pair tables out of L2
+    __stcs(eri + base + eri_pos(i, j, k, l), (ST)v);
 }
 
 // --------------------------------------------------------------------------- ERI kernels
