@@ -15,22 +15,31 @@ namespace dftb {
 
 struct XCOut { double exc, vrho, vsigma; };
 
-HD XCOut b3lyp_point(double n, double sigma) {
-    const double kPi_ = 3.14159265358979323846;
-    const double CX = 0.7385587663820223;        // 3/4 (3/pi)^(1/3)
-    const double CXS = 0.9305257363491002;       // 3/2 (3/(4 pi))^(1/3)
-    const double BETA = 0.0042;
-    const double VA = 0.0310907, VB = 13.0720, VC = 42.7198, VX0 = -0.409286;
-    const double LA = 0.04918, LB = 0.132, LC = 0.2533, LD = 0.349;
-    const double CF = 2.871234000188191;        // 0.3 (3 pi^2)^(2/3)
-    XCOut o{0.0, 0.0, 0.0};
-    n = fmax(n, 0.0);
-    sigma = fmax(sigma, 0.0);
-    if (!(n >= 1e-12)) return o;
+// The functional is evaluated in three independent parts (the device XC kernel runs them
+// on different warps) and combined by xc_combine; b3lyp_point = parts + combine, so every
+// caller performs the identical arithmetic.  Inputs are the clamped n >= 1e-12 and sigma.
+struct XPart { double f0, v0, f1, v1, w1; };      // Slater + Becke 88
+struct VPart { double f2, v2; };                  // VWN (RPA)
+struct LPart { double f3, v3, w3; };              // LYP
+
+namespace b3c {
+constexpr double kPi_ = 3.14159265358979323846;
+constexpr double CX = 0.7385587663820223;        // 3/4 (3/pi)^(1/3)
+constexpr double CXS = 0.9305257363491002;       // 3/2 (3/(4 pi))^(1/3)
+constexpr double BETA = 0.0042;
+constexpr double VA = 0.0310907, VB = 13.0720, VC = 42.7198, VX0 = -0.409286;
+constexpr double LA = 0.04918, LB = 0.132, LC = 0.2533, LD = 0.349;
+constexpr double CF = 2.871234000188191;         // 0.3 (3 pi^2)^(2/3)
+}  // namespace b3c
+
+HD XPart b3lyp_x(double n, double sigma) {
+    using namespace b3c;
+    XPart o;
     const double c13 = cbrt(n);
     // Slater exchange (per particle e = -CX n^(1/3))
     const double el = -CX * c13;
-    const double f0 = el * n, v0 = (4.0 / 3.0) * el;
+    o.f0 = el * n;
+    o.v0 = (4.0 / 3.0) * el;
     // Becke 88 on the spin density ns = n/2, sigma_s = sigma/4
     const double ns = 0.5 * n;
     const double t = cbrt(ns), t4 = t * t * t * t;
@@ -40,10 +49,15 @@ HD XCOut b3lyp_point(double n, double sigma) {
     const double dden = 6.0 * BETA * (ash + x / sqrt(1.0 + x * x));
     const double g = CXS + BETA * x * x / den;
     const double dg = BETA * (2.0 * x * den - x * x * dden) / (den * den);
-    const double f1 = -2.0 * t4 * g;
-    const double v1 = -(4.0 / 3.0) * t * g + t4 * dg * (4.0 / 3.0) * x / ns;
-    const double w1 = 0.5 * (-BETA * (2.0 * den - x * dden) / (2.0 * den * den * t4));
-    // VWN (RPA fit, paramagnetic)
+    o.f1 = -2.0 * t4 * g;
+    o.v1 = -(4.0 / 3.0) * t * g + t4 * dg * (4.0 / 3.0) * x / ns;
+    o.w1 = 0.5 * (-BETA * (2.0 * den - x * dden) / (2.0 * den * den * t4));
+    return o;
+}
+
+HD VPart b3lyp_vwn(double n) {
+    using namespace b3c;
+    VPart o;
     const double rs = cbrt(3.0 / (4.0 * kPi_ * n));
     const double y = sqrt(rs);
     const double Xy = rs + VB * y + VC;
@@ -54,8 +68,15 @@ HD XCOut b3lyp_point(double n, double sigma) {
                             (VB * VX0 / X0) * (log((y - VX0) * (y - VX0) / Xy) + (2.0 * (VB + 2.0 * VX0) / Q) * at));
     const double dec = VA * (2.0 / y - 2.0 * (y + VB) / Xy -
                              (VB * VX0 / X0) * (2.0 / (y - VX0) - 2.0 * (y + VB + VX0) / Xy));
-    const double f2 = ec * n, v2 = ec - (rs / 3.0) * dec / (2.0 * y);
-    // LYP, closed shell
+    o.f2 = ec * n;
+    o.v2 = ec - (rs / 3.0) * dec / (2.0 * y);
+    return o;
+}
+
+HD LPart b3lyp_lyp(double n, double sigma) {
+    using namespace b3c;
+    LPart o;
+    const double c13 = cbrt(n);
     const double tt = 1.0 / c13;                   // n^(-1/3)
     const double Xd = 1.0 + LD * tt;
     double tt2 = tt * tt, tt4 = tt2 * tt2, tt8 = tt4 * tt4;
@@ -63,19 +84,37 @@ HD XCOut b3lyp_point(double n, double sigma) {
     const double dl = tt * (LC + LD / Xd);
     const double n143 = n * n * n * n * cbrt(n * n);           // n^(14/3)
     const double s37 = 3.0 + 7.0 * dl;
-    const double f3 = -LA * n / Xd - LA * LB * om * CF * n143 + LA * LB * om * n * n * sigma * s37 / 72.0;
-    const double w3 = LA * LB * om * n * n * s37 / 72.0;
+    o.f3 = -LA * n / Xd - LA * LB * om * CF * n143 + LA * LB * om * n * n * sigma * s37 / 72.0;
+    o.w3 = LA * LB * om * n * n * s37 / 72.0;
     const double tp = -tt / (3.0 * n);
     const double omp = om * tp * (11.0 / tt - LC - LD / Xd);
     const double dlp = tp * (LC + LD / Xd - LD * LD * tt / (Xd * Xd));
-    const double v3 = -LA / Xd + LA * n * LD * tp / (Xd * Xd) -
-                      LA * LB * CF * (omp * n143 + om * (14.0 / 3.0) * n143 / n) +
-                      (LA * LB * sigma / 72.0) * (omp * n * n * s37 + 2.0 * n * om * s37 + 7.0 * om * n * n * dlp);
-    const double ftot = 0.08 * f0 + 0.72 * f1 + 0.19 * f2 + 0.81 * f3;
-    o.exc = ftot / n;
-    o.vrho = 0.08 * v0 + 0.72 * v1 + 0.19 * v2 + 0.81 * v3;
-    o.vsigma = 0.72 * w1 + 0.81 * w3;
+    o.v3 = -LA / Xd + LA * n * LD * tp / (Xd * Xd) -
+           LA * LB * CF * (omp * n143 + om * (14.0 / 3.0) * n143 / n) +
+           (LA * LB * sigma / 72.0) * (omp * n * n * s37 + 2.0 * n * om * s37 + 7.0 * om * n * n * dlp);
     return o;
+}
+
+HD XCOut xc_combine(double n, const XPart &x, const VPart &v, const LPart &l) {
+    XCOut o;
+    const double ftot = 0.08 * x.f0 + 0.72 * x.f1 + 0.19 * v.f2 + 0.81 * l.f3;
+    o.exc = ftot / n;
+    o.vrho = 0.08 * x.v0 + 0.72 * x.v1 + 0.19 * v.v2 + 0.81 * l.v3;
+    o.vsigma = 0.72 * x.w1 + 0.81 * l.w3;
+    return o;
+}
+
+// clamp n, sigma >= 0; zero output below n = 1e-12 (xc.py:287-290)
+HD bool b3lyp_clamp(double &n, double &sigma) {
+    n = fmax(n, 0.0);
+    sigma = fmax(sigma, 0.0);
+    return n >= 1e-12;
+}
+
+HD XCOut b3lyp_point(double n, double sigma) {
+    XCOut o{0.0, 0.0, 0.0};
+    if (!b3lyp_clamp(n, sigma)) return o;
+    return xc_combine(n, b3lyp_x(n, sigma), b3lyp_vwn(n), b3lyp_lyp(n, sigma));
 }
 
 }  // namespace dftb

@@ -12,7 +12,8 @@
 //   t = phi rho and n, grad n   4 points x 4 AOs per thread in registers, 128-bit
 //                               smem loads, partial sums reduced over the lanes
 //                               sharing the points by a shuffle tree;
-//   B3LYP                       one thread per point, f64;
+//   B3LYP                       f64; its three parts (Slater+B88, VWN, LYP) on three
+//                               groups of BP threads, combined by the first group;
 //   wv = a phi + b . grad phi   elementwise;
 //   V += phi wv^T               4 x 4 register tiles accumulated over the CTA's
 //                               whole point range, written once as a partial.
@@ -62,7 +63,8 @@ struct XCL {
     static constexpr size_t pt = wv + sizeof(W) * NP * BP;
     static constexpr size_t dn = pt + sizeof(double) * 4 * BP;
     static constexpr size_t red = dn + sizeof(double) * 4 * BP;
-    static constexpr size_t shd = red + sizeof(double) * 32;
+    static constexpr size_t fpt = red + sizeof(double) * 32;      // functional parts [10][BP]
+    static constexpr size_t shd = fpt + sizeof(double) * 10 * BP;
     static size_t bytes(int nsh) { return shd + sizeof(double) * XC_SHD * (size_t)nsh; }
 };
 
@@ -137,6 +139,7 @@ __global__ void __launch_bounds__(XC_THREADS) k_xc(DevBatch b, const int *ctas) 
     double *pt = (double *)(xsm + L::pt);
     double *dn = (double *)(xsm + L::dn);
     double *red = (double *)(xsm + L::red);
+    double *fpt = (double *)(xsm + L::fpt);
     double *shd = (double *)(xsm + L::shd);
     const int tid = threadIdx.x;
     const double *rg = b.rho + b.m_mat0[m];
@@ -239,12 +242,34 @@ __global__ void __launch_bounds__(XC_THREADS) k_xc(DevBatch b, const int *ctas) 
                 }
         }
         __syncthreads();
-        if (tid < BP) {   // ---- functional (f64), one thread per point
+        if (tid < 3 * BP) {   // ---- functional (f64): parts on three thread groups, one point each
+            const int pt_i = tid % BP, part = tid / BP;
+            const double *dq = dn + 4 * pt_i;
+            double n = dq[0], sig = 0.0;
+            {
+                const double gx = dq[1], gy = dq[2], gz = dq[3];
+                sig = (double)((W)gx * (W)gx + (W)gy * (W)gy + (W)gz * (W)gz);
+            }
+            const bool ok = pt_i < nb && b3lyp_clamp(n, sig);
+            if (part == 1) {
+                const VPart v = ok ? b3lyp_vwn(n) : VPart{0.0, 0.0};
+                fpt[5 * BP + pt_i] = v.f2;
+                fpt[6 * BP + pt_i] = v.v2;
+            } else if (part == 2) {
+                const LPart l = ok ? b3lyp_lyp(n, sig) : LPart{0.0, 0.0, 0.0};
+                fpt[7 * BP + pt_i] = l.f3;
+                fpt[8 * BP + pt_i] = l.v3;
+                fpt[9 * BP + pt_i] = l.w3;
+            }
+            XPart x{0.0, 0.0, 0.0, 0.0, 0.0};
+            if (part == 0 && ok) x = b3lyp_x(n, sig);
+            asm volatile("bar.sync 1, %0;" ::"r"(3 * BP) : "memory");
+            if (part == 0) {
             double *d = dn + 4 * tid;
-            if (tid < nb) {
-                const double n = d[0], gx = d[1], gy = d[2], gz = d[3];
-                const double sig = (double)((W)gx * (W)gx + (W)gy * (W)gy + (W)gz * (W)gz);
-                const XCOut o = b3lyp_point(n, sig);
+            if (ok) {
+                const double gx = d[1], gy = d[2], gz = d[3];
+                const XCOut o = xc_combine(n, x, VPart{fpt[5 * BP + pt_i], fpt[6 * BP + pt_i]},
+                                           LPart{fpt[7 * BP + pt_i], fpt[8 * BP + pt_i], fpt[9 * BP + pt_i]});
                 if (!(isfinite(o.exc) && isfinite(o.vrho) && isfinite(o.vsigma))) bad = 1;
                 const double w = pt[4 * tid + 3];
                 e_acc += w * n * (double)(W)o.exc;
@@ -257,6 +282,7 @@ __global__ void __launch_bounds__(XC_THREADS) k_xc(DevBatch b, const int *ctas) 
                 d[3] = bb * gz;
             } else {
                 d[0] = d[1] = d[2] = d[3] = 0.0;
+            }
             }
         }
         __syncthreads();
