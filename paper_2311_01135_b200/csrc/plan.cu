@@ -209,6 +209,13 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
     p->xcc0.assign(nm + 1, 0);
     std::vector<int> jk_mol, jk_i0, jk_i1, xc_mol;
     std::vector<int64_t> xc_p0, xc_p1;
+    int xc_main_bucket = 0;
+    {
+        int cnt[6] = {0};
+        for (int m = 0; m < nm; ++m) ++cnt[std::min(5, std::max(0, (p->nao[m] + 15) / 16 - 1))];
+        for (int k = 1; k < 6; ++k)
+            if (cnt[k] > cnt[xc_main_bucket]) xc_main_bucket = k;
+    }
     for (int m = 0; m < nm; ++m) {
         const int64_t N = p->nao[m], npp = N * (N + 1) / 2;
         p->mat0[m + 1] = p->mat0[m] + N * N;
@@ -245,11 +252,15 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
         p->grid0[m] = a_grid0[atom0[m]];
         const int64_t g_end = a_grid0[atom0[m + 1]];
         const int64_t npts = g_end - p->grid0[m];
-        const int ncx = (int)((npts + XC_CHUNK - 1) / XC_CHUNK);
+        // points per XC CTA: the most populated AO-count bucket uses XC_CHUNK; minority
+        // buckets (a few large molecules) use XC_CHUNK / 4 so their CTAs do not form a
+        // long tail behind the main launch
+        const int chunk = ((N + 15) / 16 - 1) == xc_main_bucket ? XC_CHUNK : XC_CHUNK / 4;
+        const int ncx = (int)((npts + chunk - 1) / chunk);
         for (int c = 0; c < ncx; ++c) {
             xc_mol.push_back(m);
-            xc_p0.push_back(p->grid0[m] + (int64_t)c * XC_CHUNK);
-            xc_p1.push_back(std::min(g_end, p->grid0[m] + (int64_t)(c + 1) * XC_CHUNK));
+            xc_p0.push_back(p->grid0[m] + (int64_t)c * chunk);
+            xc_p1.push_back(std::min(g_end, p->grid0[m] + (int64_t)(c + 1) * chunk));
         }
         p->xcc0[m + 1] = p->xcc0[m] + ncx;
         V0[m + 1] = V0[m] + (int64_t)ncx * N * N;
