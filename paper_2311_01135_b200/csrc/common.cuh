@@ -85,6 +85,7 @@ struct DevBatch {
     double *qao;              // [sum npp] sqrt((ij|ij))
     // J/K CTA table
     const int *jk_mol, *jk_i0, *jk_i1;
+    const int *mol_order;     // molecules by N descending: launch order of the per-molecule kernels
     int n_jk_cta;
     // XC CTA table
     const int *xc_mol;

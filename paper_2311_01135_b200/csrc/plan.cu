@@ -283,6 +283,28 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
         p->jk_bucket_n[bkt] = (int)(jk_sorted.size() - before);
     }
     p->eri0 = eri0;
+    // largest molecules first: the per-molecule SCF kernels run ~2 waves of one CTA per SM,
+    // so longest-first keeps the second wave from ending on a large molecule
+    std::vector<int> mol_order(nm);
+    for (int m = 0; m < nm; ++m) mol_order[m] = m;
+    std::stable_sort(mol_order.begin(), mol_order.end(), [&](int a, int c) { return p->nao[a] > p->nao[c]; });
+    // J/K CTAs: largest work first within each bucket
+    {
+        auto work = [&](int c) {
+            int64_t w = 0;
+            for (int i = jk_i0[c]; i < jk_i1[c]; ++i) {
+                const int64_t A = i / 4 + 1;
+                w += (int64_t)(i + 1) * (A * (A + 1) / 2);
+            }
+            return w;
+        };
+        int off = 0;
+        for (int bkt = 0; bkt < 6; ++bkt) {
+            std::stable_sort(jk_sorted.begin() + off, jk_sorted.begin() + off + p->jk_bucket_n[bkt],
+                             [&](int a, int c) { return work(a) > work(c); });
+            off += p->jk_bucket_n[bkt];
+        }
+    }
     const int64_t npts_tot = a_grid0[in->n_atom];
     const int njk = (int)jk_mol.size(), nxc = (int)xc_mol.size();
     const int64_t mat = p->mat0[nm];
@@ -336,6 +358,7 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
     UP(jk_i0, int, jk_i0.data(), njk)
     UP(jk_i1, int, jk_i1.data(), njk)
     UP(jk_sorted, int, jk_sorted.data(), njk)
+    UP(mol_order, int, mol_order.data(), nm)
     UP(xc_mol, int, xc_mol.data(), nxc)
     UP(xc_p0, int64_t, xc_p0.data(), nxc)
     UP(xc_p1, int64_t, xc_p1.data(), nxc)
@@ -429,6 +452,7 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
     d.n_xc_cta = nxc;
     p->xc_bucket_ctas = PTR(int, o_xc_sorted);
     p->jk_bucket_ctas = PTR(int, o_jk_sorted);
+    d.mol_order = PTR(int, o_mol_order);
     d.g_xyz = PTR(double, o_gxyz); d.g_w = PTR(double, o_gw);
     double **mats[14] = {&d.S, &d.T, &d.V, &d.H, &d.X, &d.C, &d.Cp, &d.rho, &d.rho_prev, &d.F, &d.J, &d.K, &d.Vxc,
                          &d.scratch};

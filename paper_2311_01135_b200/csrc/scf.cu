@@ -307,7 +307,7 @@ __device__ void sort_dv(int n, const Arena &ar) {
 __global__ void __launch_bounds__(SCF_THREADS, 2) k_orth(DevBatch b, int nm) {
     extern __shared__ __align__(16) unsigned char ssm[];
     const Arena ar = carve(ssm, nm);
-    const int m = blockIdx.x, N = b.m_nao[m], tid = threadIdx.x;
+    const int m = b.mol_order[blockIdx.x], N = b.m_nao[m], tid = threadIdx.x;
     const int64_t o = b.m_mat0[m];
     for (int t = tid; t < N * N; t += SCF_THREADS) {
         ar.A[t] = b.S[o + t];
@@ -512,7 +512,7 @@ __device__ void diis_extrapolate(const DevBatch &b, int m, int N, const double *
 __global__ void __launch_bounds__(SCF_THREADS, 2) k_post(DevBatch b, PostArgs pa) {
     extern __shared__ __align__(16) unsigned char ssm[];
     const Arena ar = carve(ssm, pa.nm);
-    const int m = blockIdx.x, tid = threadIdx.x;
+    const int m = b.mol_order[blockIdx.x], tid = threadIdx.x;
     if (b.done[m]) return;
     const int N = b.m_nao[m], M = b.nmo[m], nocc = b.m_nocc[m];
     if (b.status[m] & (DFTB_ST_OVERLAP_NOT_PD | DFTB_ST_NO_ORBITALS)) {
@@ -611,8 +611,10 @@ __global__ void __launch_bounds__(SCF_THREADS, 2) k_post(DevBatch b, PostArgs pa
     }
     __syncthreads();
     {
+        // f32 build: eigenvectors to f32 resolution (the reference's f32 path diagonalizes in
+        // single precision, scf.py:86-98); f64 build: to 1e-13 of the largest |eigenvalue|
         int nsw = 0;
-        Ad = cta_jacobi(ar.A, ar.W, ar.B, M, ar, &nsw);
+        Ad = cta_jacobi(ar.A, ar.W, ar.B, M, ar, &nsw, 30, b.prec ? 1e-8 : 1e-13);
         if (dbg && tid == 0) dbg[10] += nsw;
     }
     tick(4);
@@ -680,7 +682,7 @@ void launch_post(const DevBatch &b, int nmax, int it, int diis_start, int diis_h
 __global__ void __launch_bounds__(SCF_THREADS) k_roothaan(DevBatch b, int nm) {
     extern __shared__ __align__(16) unsigned char ssm[];
     const Arena ar = carve(ssm, nm);
-    const int m = blockIdx.x, tid = threadIdx.x;
+    const int m = b.mol_order[blockIdx.x], tid = threadIdx.x;
     const int N = b.m_nao[m], M = b.nmo[m];
     const int64_t o = b.m_mat0[m], tot = b.m_mat0[b.n_mol];
     double *X = b.X + o, *C = b.C + o, *Cp = b.Cp + o, *S2 = b.scratch + tot + o;
