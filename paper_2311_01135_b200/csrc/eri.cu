@@ -117,9 +117,25 @@ __device__ __forceinline__ void store_eri(ST *eri, int64_t base, int i, int j, i
 }
 
 // --------------------------------------------------------------------------- ERI kernels
+// Per-thread shared-memory copy of the ket pair's nine primitive records: the primitive
+// loop reads each ket record once per bra primitive (81 times per quartet), so keeping them
+// next to the SM removes ~8/9 of the kernel's load traffic.  Slots [slot][prim][thread];
+// S-only kets need 7 fields (the screening bound goes to slot 6).
+constexpr int ERI_T = 128;
+template <bool LKET>
+struct KetSmem {
+    static constexpr int NSLOT = LKET ? 10 : 7;
+    const double *s;
+    int lane;
+    __device__ __forceinline__ static int slot(int f) { return (!LKET && f == PF_BOUND) ? 6 : f; }
+    __device__ __forceinline__ double get(int f, int k, int64_t) const {
+        return s[(slot(f) * 9 + k) * ERI_T + lane];
+    }
+};
+
 // One thread = one screened shell quartet x one ket-component slice (blockIdx.y).
 template <int KA, int KB, int KC, int KD, int SPLIT, typename ST>
-__global__ void __launch_bounds__(128) k_eri(DevBatch b, int cls, double eps, double prim_cut, ST *eri) {
+__global__ void __launch_bounds__(ERI_T) k_eri(DevBatch b, int cls, double eps, double prim_cut, ST *eri) {
     constexpr int NA = KA ? 4 : 1, NB = KB ? 4 : 1, NC = KC ? 4 : 1, ND = KD ? 4 : 1;
     constexpr int NKET = NC * ND, NKS = SPLIT ? 1 : NKET, NSL = NKET / NKS;
     const int64_t *pre = b.cls0 + (int64_t)cls * (b.n_mol + 1);
@@ -136,6 +152,15 @@ __global__ void __launch_bounds__(128) k_eri(DevBatch b, int cls, double eps, do
     load_geo(b, Pp, A, B);
     load_geo(b, Qp, C, D);
     const PPView V{b.pp, b.n_pair};
+    extern __shared__ double eri_ksm[];
+    using KS = KetSmem<(KC || KD)>;
+    const KS VK{eri_ksm, (int)threadIdx.x};
+#pragma unroll
+    for (int f = 0; f < KS::NSLOT; ++f) {
+        const int field = (f == 6 && !(KC || KD)) ? (int)PF_BOUND : f;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) eri_ksm[(f * 9 + k) * ERI_T + threadIdx.x] = V.get(field, k, Qp);
+    }
     const int ia = b.s_ao[b.p_sa[Pp]], ib = b.s_ao[b.p_sb[Pp]];
     const int ic = b.s_ao[b.p_sa[Qp]], id = b.s_ao[b.p_sb[Qp]];
     const int64_t base = b.m_eri0[m];
@@ -146,7 +171,7 @@ __global__ void __launch_bounds__(128) k_eri(DevBatch b, int cls, double eps, do
         for (int x = 0; x < NA * NB; ++x)
 #pragma unroll
             for (int y = 0; y < NKS; ++y) out[x][y] = 0.0;
-        eri_quartet<KA, KB, KC, KD, KC0, NKS>(V, Pp, Qp, A, B, C, D, b.boys, prim_cut, out);
+        eri_quartet_kv<KA, KB, KC, KD, KC0, NKS>(V, VK, Pp, Qp, A, B, C, D, b.boys, prim_cut, out);
         // single writer per canonical element: for a diagonal shell pair only the
         // (i >= j) component writes, for a diagonal quartet only the (ij >= kl) image
         const bool dab = b.p_sa[Pp] == b.p_sb[Pp], dcd = b.p_sa[Qp] == b.p_sb[Qp], dpq = Pp == Qp;
@@ -235,16 +260,25 @@ void launch_schwarz(const DevBatch &b, const int64_t *host_totals, cudaStream_t 
     if (b.n_pair) k_pair_q<<<nblk(b.n_pair, 128), 128, 0, s>>>(b);
 }
 
+template <int KA, int KB, int KC, int KD, int SPLIT, typename ST>
+static void launch_cls(const DevBatch &b, int cls, int64_t n, int slices, double eps, double prim_cut, ST *eri,
+                       cudaStream_t s, int *nlaunch) {
+    if (!n) return;
+    const size_t sm = sizeof(double) * KetSmem<(KC || KD)>::NSLOT * 9 * ERI_T;
+    cudaFuncSetAttribute(k_eri<KA, KB, KC, KD, SPLIT, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_eri<KA, KB, KC, KD, SPLIT, ST><<<dim3(nblk(n, ERI_T), slices), ERI_T, sm, s>>>(b, cls, eps, prim_cut, eri);
+    ++*nlaunch;
+}
+
 template <typename ST>
 static void launch_eri_t(const DevBatch &b, const int64_t *tot, double eps, double prim_cut,
                          ST *eri, cudaStream_t s, int *nlaunch) {
-    const int T = 128;
-    if (tot[0]) { k_eri<1, 1, 1, 1, 1, ST><<<dim3(nblk(tot[0], T), 16), T, 0, s>>>(b, 0, eps, prim_cut, eri); ++*nlaunch; }
-    if (tot[1]) { k_eri<1, 1, 1, 0, 1, ST><<<dim3(nblk(tot[1], T), 4), T, 0, s>>>(b, 1, eps, prim_cut, eri); ++*nlaunch; }
-    if (tot[2]) { k_eri<1, 1, 0, 0, 0, ST><<<dim3(nblk(tot[2], T), 1), T, 0, s>>>(b, 2, eps, prim_cut, eri); ++*nlaunch; }
-    if (tot[3]) { k_eri<1, 0, 1, 0, 0, ST><<<dim3(nblk(tot[3], T), 1), T, 0, s>>>(b, 3, eps, prim_cut, eri); ++*nlaunch; }
-    if (tot[4]) { k_eri<1, 0, 0, 0, 0, ST><<<dim3(nblk(tot[4], T), 1), T, 0, s>>>(b, 4, eps, prim_cut, eri); ++*nlaunch; }
-    if (tot[5]) { k_eri<0, 0, 0, 0, 0, ST><<<dim3(nblk(tot[5], T), 1), T, 0, s>>>(b, 5, eps, prim_cut, eri); ++*nlaunch; }
+    launch_cls<1, 1, 1, 1, 1>(b, 0, tot[0], 16, eps, prim_cut, eri, s, nlaunch);
+    launch_cls<1, 1, 1, 0, 1>(b, 1, tot[1], 4, eps, prim_cut, eri, s, nlaunch);
+    launch_cls<1, 1, 0, 0, 0>(b, 2, tot[2], 1, eps, prim_cut, eri, s, nlaunch);
+    launch_cls<1, 0, 1, 0, 0>(b, 3, tot[3], 1, eps, prim_cut, eri, s, nlaunch);
+    launch_cls<1, 0, 0, 0, 0>(b, 4, tot[4], 1, eps, prim_cut, eri, s, nlaunch);
+    launch_cls<0, 0, 0, 0, 0>(b, 5, tot[5], 1, eps, prim_cut, eri, s, nlaunch);
 }
 
 void launch_eri(const DevBatch &b, const int64_t *tot, double eps, double prim_cut, cudaStream_t s,

@@ -132,10 +132,12 @@ HD void e1d(int la, int lb, double pa, double pb, double h, double *e) {
 // (ab|cd) for all bra components x ket components [KC0, KC0+NKS).  Kinds: 0 = S, 1 = L.
 // out[bc][k] accumulates (caller zeroes).  prim_cut > 0 skips primitive quartets with
 // pref * bound_ab * bound_cd < prim_cut (the reference's primitive screen, _kernels.py:376-377).
-template <int KA, int KB, int KC, int KD, int KC0, int NKS>
-HD void eri_quartet(const PPView &V, int64_t Pp, int64_t Qp, const double *A, const double *B,
-                    const double *C, const double *D, const double *tab, double prim_cut,
-                    double (*out)[NKS]) {
+// V: bra primitive-pair records; VK: the ket's (any view with get(field, prim, pair); the
+// device ERI kernel passes a per-thread shared-memory copy of its ket's nine records).
+template <int KA, int KB, int KC, int KD, int KC0, int NKS, typename KV>
+HD void eri_quartet_kv(const PPView &V, const KV &VK, int64_t Pp, int64_t Qp, const double *A,
+                       const double *B, const double *C, const double *D, const double *tab,
+                       double prim_cut, double (*out)[NKS]) {
     constexpr int NA = KA ? 4 : 1, NB = KB ? 4 : 1, ND = KD ? 4 : 1;
     constexpr int LB = KA + KB, LK = KC + KD, L = LB + LK;
     constexpr int NHB = nherm(LB);
@@ -150,22 +152,22 @@ HD void eri_quartet(const PPView &V, int64_t Pp, int64_t Qp, const double *A, co
 #pragma unroll
             for (int k = 0; k < NKS; ++k) W[h][k] = 0.0;
         for (int ik = 0; ik < 9; ++ik) {
-            const double q = V.get(PF_P, ik, Qp);
-            const double hq = V.get(PF_H, ik, Qp);
+            const double q = VK.get(PF_P, ik, Qp);
+            const double hq = VK.get(PF_H, ik, Qp);
             const double r = drsqrt(p + q);
             const double pref = kTwoPi25 * (4.0 * hp * hq) * r;  // 2 pi^2.5 / (p q sqrt(p+q))
-            if (prim_cut > 0.0 && pref * bb * V.get(PF_BOUND, ik, Qp) < prim_cut) continue;
-            const double Qx = V.get(PF_X, ik, Qp), Qy = V.get(PF_Y, ik, Qp), Qz = V.get(PF_Z, ik, Qp);
+            if (prim_cut > 0.0 && pref * bb * VK.get(PF_BOUND, ik, Qp) < prim_cut) continue;
+            const double Qx = VK.get(PF_X, ik, Qp), Qy = VK.get(PF_Y, ik, Qp), Qz = VK.get(PF_Z, ik, Qp);
             const double alpha = p * q * (r * r);
             const double X = Px - Qx, Y = Py - Qy, Z = Pz - Qz;
             double R[nherm(L)];
             hermite_R<L>(alpha * (X * X + Y * Y + Z * Z), alpha, X, Y, Z, pref, tab, R);
             double ck[4];
-            ck[0] = V.get(PF_CSS, ik, Qp);
+            ck[0] = VK.get(PF_CSS, ik, Qp);
             if (KC || KD) {
-                ck[1] = V.get(PF_CSP, ik, Qp);
-                ck[2] = V.get(PF_CPS, ik, Qp);
-                ck[3] = V.get(PF_CPP, ik, Qp);
+                ck[1] = VK.get(PF_CSP, ik, Qp);
+                ck[2] = VK.get(PF_CPS, ik, Qp);
+                ck[3] = VK.get(PF_CPP, ik, Qp);
             }
             const double QC[3] = {Qx - C[0], Qy - C[1], Qz - C[2]};
             const double QD[3] = {Qx - D[0], Qy - D[1], Qz - D[2]};
@@ -240,6 +242,13 @@ HD void eri_quartet(const PPView &V, int64_t Pp, int64_t Qp, const double *A, co
             }
         }
     }
+}
+
+template <int KA, int KB, int KC, int KD, int KC0, int NKS>
+HD void eri_quartet(const PPView &V, int64_t Pp, int64_t Qp, const double *A, const double *B,
+                    const double *C, const double *D, const double *tab, double prim_cut,
+                    double (*out)[NKS]) {
+    eri_quartet_kv<KA, KB, KC, KD, KC0, NKS>(V, V, Pp, Qp, A, B, C, D, tab, prim_cut, out);
 }
 
 // ---------------------------------------------------------------------------- one-electron
