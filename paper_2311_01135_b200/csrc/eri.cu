@@ -134,10 +134,13 @@ struct KetSmem {
 };
 
 // One thread = one screened shell quartet x one ket-component slice (blockIdx.y).
-template <int KA, int KB, int KC, int KD, int SPLIT, typename ST>
+// KPS: ket components per slice (0 = all): a slice recomputes the Boys function and
+// R_tuv of all 81 primitive quartets, so fewer slices trade registers for less recomputation.
+template <int KA, int KB, int KC, int KD, int KPS, typename ST>
 __global__ void __launch_bounds__(ERI_T) k_eri(DevBatch b, int cls, double eps, double prim_cut, ST *eri) {
     constexpr int NA = KA ? 4 : 1, NB = KB ? 4 : 1, NC = KC ? 4 : 1, ND = KD ? 4 : 1;
-    constexpr int NKET = NC * ND, NKS = SPLIT ? 1 : NKET, NSL = NKET / NKS;
+    constexpr int NKET = NC * ND, NKS = KPS ? KPS : NKET, NSL = NKET / NKS;
+    static_assert(NKET % NKS == 0, "slice size must divide the ket component count");
     const int64_t *pre = b.cls0 + (int64_t)cls * (b.n_mol + 1);
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= pre[b.n_mol]) return;
@@ -260,25 +263,33 @@ void launch_schwarz(const DevBatch &b, const int64_t *host_totals, cudaStream_t 
     if (b.n_pair) k_pair_q<<<nblk(b.n_pair, 128), 128, 0, s>>>(b);
 }
 
-template <int KA, int KB, int KC, int KD, int SPLIT, typename ST>
-static void launch_cls(const DevBatch &b, int cls, int64_t n, int slices, double eps, double prim_cut, ST *eri,
+template <int KA, int KB, int KC, int KD, int KPS, typename ST>
+static void launch_cls(const DevBatch &b, int cls, int64_t n, double eps, double prim_cut, ST *eri,
                        cudaStream_t s, int *nlaunch) {
     if (!n) return;
+    constexpr int NKET = (KC ? 4 : 1) * (KD ? 4 : 1), NSL = NKET / (KPS ? KPS : NKET);
     const size_t sm = sizeof(double) * KetSmem<(KC || KD)>::NSLOT * 9 * ERI_T;
-    cudaFuncSetAttribute(k_eri<KA, KB, KC, KD, SPLIT, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_eri<KA, KB, KC, KD, SPLIT, ST><<<dim3(nblk(n, ERI_T), slices), ERI_T, sm, s>>>(b, cls, eps, prim_cut, eri);
+    cudaFuncSetAttribute(k_eri<KA, KB, KC, KD, KPS, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_eri<KA, KB, KC, KD, KPS, ST><<<dim3(nblk(n, ERI_T), NSL), ERI_T, sm, s>>>(b, cls, eps, prim_cut, eri);
     ++*nlaunch;
 }
+
+#ifndef ERI_KPS_LL
+#define ERI_KPS_LL 2       // LL|LL: 8 slices of 2 ket components
+#endif
+#ifndef ERI_KPS_LS
+#define ERI_KPS_LS 2       // LL|LS: 2 slices of 2
+#endif
 
 template <typename ST>
 static void launch_eri_t(const DevBatch &b, const int64_t *tot, double eps, double prim_cut,
                          ST *eri, cudaStream_t s, int *nlaunch) {
-    launch_cls<1, 1, 1, 1, 1>(b, 0, tot[0], 16, eps, prim_cut, eri, s, nlaunch);
-    launch_cls<1, 1, 1, 0, 1>(b, 1, tot[1], 4, eps, prim_cut, eri, s, nlaunch);
-    launch_cls<1, 1, 0, 0, 0>(b, 2, tot[2], 1, eps, prim_cut, eri, s, nlaunch);
-    launch_cls<1, 0, 1, 0, 0>(b, 3, tot[3], 1, eps, prim_cut, eri, s, nlaunch);
-    launch_cls<1, 0, 0, 0, 0>(b, 4, tot[4], 1, eps, prim_cut, eri, s, nlaunch);
-    launch_cls<0, 0, 0, 0, 0>(b, 5, tot[5], 1, eps, prim_cut, eri, s, nlaunch);
+    launch_cls<1, 1, 1, 1, ERI_KPS_LL>(b, 0, tot[0], eps, prim_cut, eri, s, nlaunch);
+    launch_cls<1, 1, 1, 0, ERI_KPS_LS>(b, 1, tot[1], eps, prim_cut, eri, s, nlaunch);
+    launch_cls<1, 1, 0, 0, 0>(b, 2, tot[2], eps, prim_cut, eri, s, nlaunch);
+    launch_cls<1, 0, 1, 0, 0>(b, 3, tot[3], eps, prim_cut, eri, s, nlaunch);
+    launch_cls<1, 0, 0, 0, 0>(b, 4, tot[4], eps, prim_cut, eri, s, nlaunch);
+    launch_cls<0, 0, 0, 0, 0>(b, 5, tot[5], eps, prim_cut, eri, s, nlaunch);
 }
 
 void launch_eri(const DevBatch &b, const int64_t *tot, double eps, double prim_cut, cudaStream_t s,
