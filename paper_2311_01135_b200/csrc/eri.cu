@@ -136,7 +136,9 @@ struct KetSmem {
 // One thread = one screened shell quartet x one ket-component slice (blockIdx.y).
 // KPS: ket components per slice (0 = all): a slice recomputes the Boys function and
 // R_tuv of all 81 primitive quartets, so fewer slices trade registers for less recomputation.
-template <int KA, int KB, int KC, int KD, int KPS, typename ST>
+// KSM: keep the ket records in shared memory (off for SS|SS, whose occupancy it would cut
+// from 9 to 3 CTAs per SM for a class that is cheap per primitive quartet)
+template <int KA, int KB, int KC, int KD, int KPS, typename ST, bool KSM = true>
 __global__ void __launch_bounds__(ERI_T) k_eri(DevBatch b, int cls, double eps, double prim_cut, ST *eri) {
     constexpr int NA = KA ? 4 : 1, NB = KB ? 4 : 1, NC = KC ? 4 : 1, ND = KD ? 4 : 1;
     constexpr int NKET = NC * ND, NKS = KPS ? KPS : NKET, NSL = NKET / NKS;
@@ -158,11 +160,13 @@ __global__ void __launch_bounds__(ERI_T) k_eri(DevBatch b, int cls, double eps, 
     extern __shared__ double eri_ksm[];
     using KS = KetSmem<(KC || KD)>;
     const KS VK{eri_ksm, (int)threadIdx.x};
+    if constexpr (KSM) {
 #pragma unroll
-    for (int f = 0; f < KS::NSLOT; ++f) {
-        const int field = (f == 6 && !(KC || KD)) ? (int)PF_BOUND : f;
+        for (int f = 0; f < KS::NSLOT; ++f) {
+            const int field = (f == 6 && !(KC || KD)) ? (int)PF_BOUND : f;
 #pragma unroll
-        for (int k = 0; k < 9; ++k) eri_ksm[(f * 9 + k) * ERI_T + threadIdx.x] = V.get(field, k, Qp);
+            for (int k = 0; k < 9; ++k) eri_ksm[(f * 9 + k) * ERI_T + threadIdx.x] = V.get(field, k, Qp);
+        }
     }
     const int ia = b.s_ao[b.p_sa[Pp]], ib = b.s_ao[b.p_sb[Pp]];
     const int ic = b.s_ao[b.p_sa[Qp]], id = b.s_ao[b.p_sb[Qp]];
@@ -174,7 +178,8 @@ __global__ void __launch_bounds__(ERI_T) k_eri(DevBatch b, int cls, double eps, 
         for (int x = 0; x < NA * NB; ++x)
 #pragma unroll
             for (int y = 0; y < NKS; ++y) out[x][y] = 0.0;
-        eri_quartet_kv<KA, KB, KC, KD, KC0, NKS>(V, VK, Pp, Qp, A, B, C, D, b.boys, prim_cut, out);
+        if constexpr (KSM) eri_quartet_kv<KA, KB, KC, KD, KC0, NKS>(V, VK, Pp, Qp, A, B, C, D, b.boys, prim_cut, out);
+        else eri_quartet_kv<KA, KB, KC, KD, KC0, NKS>(V, V, Pp, Qp, A, B, C, D, b.boys, prim_cut, out);
         // single writer per canonical element: for a diagonal shell pair only the
         // (i >= j) component writes, for a diagonal quartet only the (ij >= kl) image
         const bool dab = b.p_sa[Pp] == b.p_sb[Pp], dcd = b.p_sa[Qp] == b.p_sb[Qp], dpq = Pp == Qp;
@@ -263,14 +268,15 @@ void launch_schwarz(const DevBatch &b, const int64_t *host_totals, cudaStream_t 
     if (b.n_pair) k_pair_q<<<nblk(b.n_pair, 128), 128, 0, s>>>(b);
 }
 
-template <int KA, int KB, int KC, int KD, int KPS, typename ST>
+template <int KA, int KB, int KC, int KD, int KPS, bool KSM = true, typename ST>
 static void launch_cls(const DevBatch &b, int cls, int64_t n, double eps, double prim_cut, ST *eri,
                        cudaStream_t s, int *nlaunch) {
     if (!n) return;
     constexpr int NKET = (KC ? 4 : 1) * (KD ? 4 : 1), NSL = NKET / (KPS ? KPS : NKET);
-    const size_t sm = sizeof(double) * KetSmem<(KC || KD)>::NSLOT * 9 * ERI_T;
-    cudaFuncSetAttribute(k_eri<KA, KB, KC, KD, KPS, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_eri<KA, KB, KC, KD, KPS, ST><<<dim3(nblk(n, ERI_T), NSL), ERI_T, sm, s>>>(b, cls, eps, prim_cut, eri);
+    const size_t sm = KSM ? sizeof(double) * KetSmem<(KC || KD)>::NSLOT * 9 * ERI_T : 0;
+    auto kern = k_eri<KA, KB, KC, KD, KPS, ST, KSM>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kern<<<dim3(nblk(n, ERI_T), NSL), ERI_T, sm, s>>>(b, cls, eps, prim_cut, eri);
     ++*nlaunch;
 }
 
@@ -289,7 +295,7 @@ static void launch_eri_t(const DevBatch &b, const int64_t *tot, double eps, doub
     launch_cls<1, 1, 0, 0, 0>(b, 2, tot[2], eps, prim_cut, eri, s, nlaunch);
     launch_cls<1, 0, 1, 0, 0>(b, 3, tot[3], eps, prim_cut, eri, s, nlaunch);
     launch_cls<1, 0, 0, 0, 0>(b, 4, tot[4], eps, prim_cut, eri, s, nlaunch);
-    launch_cls<0, 0, 0, 0, 0>(b, 5, tot[5], eps, prim_cut, eri, s, nlaunch);
+    launch_cls<0, 0, 0, 0, 0, false>(b, 5, tot[5], eps, prim_cut, eri, s, nlaunch);
 }
 
 void launch_eri(const DevBatch &b, const int64_t *tot, double eps, double prim_cut, cudaStream_t s,
