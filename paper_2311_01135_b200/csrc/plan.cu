@@ -511,6 +511,16 @@ int dftb_plan_set_timing(dftb_plan *p, int enable) {
     return 0;
 }
 
+// fork: aux waits for everything issued on st so far; join: st waits for aux
+static cudaError_t fork(dftb_plan *p, cudaStream_t st) {
+    cudaError_t e = cudaEventRecord(p->fork, st);
+    return e != cudaSuccess ? e : cudaStreamWaitEvent(p->aux, p->fork, 0);
+}
+static cudaError_t join(dftb_plan *p, cudaStream_t st) {
+    cudaError_t e = cudaEventRecord(p->join, p->aux);
+    return e != cudaSuccess ? e : cudaStreamWaitEvent(st, p->join, 0);
+}
+
 int dftb_plan_begin(dftb_plan *p, void *stream) {
     if (!p) return fail(DFTB_EINVAL, "null plan");
     cudaStream_t st = (cudaStream_t)stream;
@@ -519,16 +529,21 @@ int dftb_plan_begin(dftb_plan *p, void *stream) {
     int rc = zero_work(p, st);
     if (rc) return rc;
     mark(p, 0, st);
+    // the one-electron integrals, grid, orthogonaliser and core guess do not depend on the
+    // ERI stage: they run on the aux stream while the pair tables, Schwarz bounds and ERIs
+    // run on the caller's stream (stage 1 = ERI stage, stage 2 = the wait for the rest)
+    CK(fork(p, st));
+    launch_onee(d, p->aux);
+    launch_enn(d, p->aux);
+    launch_grid(d, p->natom_max, p->aux);
+    launch_orth(d, p->nmax, p->aux);
+    const dftb_opts &o = p->opts;
+    launch_post(d, p->nmax, -1, o.diis_start, o.diis_history, o.damping_factor, o.convergence_std, p->aux);
+    p->launches += 5;
     rc = setup_stage(p, st, true);
     if (rc) return rc;
     mark(p, 1, st);
-    launch_onee(d, st);
-    launch_enn(d, st);
-    launch_grid(d, p->natom_max, st);
-    launch_orth(d, p->nmax, st);
-    const dftb_opts &o = p->opts;
-    launch_post(d, p->nmax, -1, o.diis_start, o.diis_history, o.damping_factor, o.convergence_std, st);
-    p->launches += 5;
+    CK(join(p, st));
     CK(cudaGetLastError());
     mark(p, 2, st);
     return 0;
@@ -541,12 +556,10 @@ int dftb_plan_iterate(dftb_plan *p, int32_t it, void *stream) {
     const dftb_opts &o = p->opts;
     // J/K (aux stream) and XC (caller's stream) both read rho and write separate partials:
     // fork/join so their CTAs share the SMs (FP64/XU-heavy vs FP32-heavy, smem fits both)
-    CK(cudaEventRecord(p->fork, st));
-    CK(cudaStreamWaitEvent(p->aux, p->fork, 0));
+    CK(fork(p, st));
     const int njl = launch_jk(d, p->jk_bucket_ctas, p->jk_bucket_n, p->aux);
     const int nxl = launch_xc(d, p->xc_bucket_ctas, p->xc_bucket_n, p->nsh_max, st);
-    CK(cudaEventRecord(p->join, p->aux));
-    CK(cudaStreamWaitEvent(st, p->join, 0));
+    CK(join(p, st));
     launch_post(d, p->nmax, it, o.diis_start, o.diis_history, o.damping_factor, o.convergence_std, st);
     p->launches += 1 + njl + nxl;
     CK(cudaGetLastError());
