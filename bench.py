@@ -227,6 +227,16 @@ def run_reference(args, ws, rank):
 
 
 # ----------------------------------------------------------------------------- GPU arm
+def _hbm_peak():
+    """HBM copy bandwidth measured on this pool (MEASURED_PEAKS.json, burst), else the
+    profiling recipe's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (burst copy)"
+    except (OSError, KeyError, ValueError):
+        return 7700.0, "B200_PROFILING.md fallback (HBM3e nominal)"
+
+
 def _eri_traffic():
     """DRAM bytes (read + write) of one step's ERI stage from the committed ncu --set full
     capture (profiles/r1_eri_traffic.json), or None when the summary is absent."""
@@ -328,6 +338,16 @@ def run_ours(args, ws, rank, local):
     eri_ms = stage[0]
     achieved = float(np.mean([f / (p_.stage_times()[0] / 1000.0) for f, p_ in zip(flops_all[:len(used)], used)])) / 1e12
     achieved_iso = flops / (iso_stage[0] / 1000.0) / 1e12
+    # ---------------- XC and J/K kernels against their own rooflines (re-run on the resident density)
+    ms_jk, ms_xc = plan.kernel_times(5)
+    nao = np.asarray(plan.pk.mol_nao, dtype=np.float64)
+    npts = np.asarray(plan.pk.mol_npts, dtype=np.float64)
+    xc_flops = float(np.sum(4.0 * nao * nao * npts))            # two N^2 contractions per grid point
+    peak32 = ctypes.c_double(0.0)
+    _lib.check(lib.dftb_fma_peak(0, ctypes.byref(peak32), sp))
+    xc_tf = xc_flops / (ms_xc / 1000.0) / 1e12
+    jk_gbs = info["eri_bytes"] / (ms_jk / 1000.0) / 1e9
+    hbm_peak, hbm_src = _hbm_peak()
     n_ao_mean = float(np.mean(plan.pk.mol_nao))
     mol_nao_sq = int(sum(int(x) ** 2 for x in plan.pk.mol_nao))
     for p_ in plans:
@@ -377,6 +397,17 @@ def run_ours(args, ws, rank, local):
                                     "(MEASURED_PEAKS.json has no FP64 figure)",
                      "timing": f"ERI-stage CUDA events over the timed region ({F} batches in flight, so the "
                                "stage shares the SMs with other batches' SCF loops)"},
+        "roofline_xc": {"kernel": "k_xc (AO values + density + B3LYP + V_xc, f32 contractions)", "bound": "fp32",
+                        "achieved": xc_tf, "peak": peak32.value, "unit": "TFLOP/s",
+                        "frac": xc_tf / peak32.value if peak32.value else None, "ms_per_iteration": ms_xc,
+                        "algorithmic": "4 N^2 flops per grid point per iteration (phi^T rho and phi wv^T), "
+                                       f"{xc_flops / 1e9:.1f} GFLOP per iteration",
+                        "peak_source": "measured: dftb_fma_peak FP32 FFMA probe on this GPU"},
+        "roofline_jk": {"kernel": "k_jk (J/K digestion of the ERI store)", "bound": "hbm",
+                        "achieved": jk_gbs, "peak": hbm_peak, "unit": "GB/s",
+                        "frac": jk_gbs / hbm_peak if hbm_peak else None, "ms_per_iteration": ms_jk,
+                        "algorithmic": f"the {info['eri_bytes'] / 2**30:.2f} GiB ERI store read once per iteration",
+                        "peak_source": hbm_src},
         "roofline_isolated": {"achieved": achieved_iso, "peak": peak.value, "unit": "TFLOP/s",
                               "frac": achieved_iso / peak.value if peak.value else None,
                               "timing": "same ERI stage, one batch alone on the GPU (warm-up pass)"},

@@ -157,6 +157,11 @@ int dftb_plan_launch_count(const dftb_plan *plan, int64_t *count);
 int dftb_plan_set_timing(dftb_plan *plan, int enable);
 /* Measured-peak helper: FP64 / FP32 FMA throughput microbenchmark (TFLOP/s). */
 int dftb_fma_peak(int fp64, double *tflops, void *stream);
+/* Kernel-level timing for roofline reporting: re-runs the J/K digestion and the XC
+ * kernels (pure functions of the device-resident density; they only rewrite their own
+ * partials) `reps` times between CUDA events on `stream` and returns the average time of
+ * one J/K launch set and of one XC launch set (ms).  Requires a completed dftb_plan_run. */
+int dftb_plan_kernel_times(dftb_plan *plan, int32_t reps, double *ms_jk, double *ms_xc, void *stream);
 
 #ifdef __cplusplus
 }

@@ -116,6 +116,13 @@ class Plan:
     def iterate(self, it: int):
         _lib.check(self.lib.dftb_plan_iterate(self.h, int(it), self.stream))
 
+    def kernel_times(self, reps: int = 5) -> tuple[float, float]:
+        """(ms per J/K launch set, ms per XC launch set) re-run on the resident density."""
+        jk, xc = ctypes.c_double(0.0), ctypes.c_double(0.0)
+        _lib.check(self.lib.dftb_plan_kernel_times(self.h, int(reps), ctypes.byref(jk), ctypes.byref(xc),
+                                                   self.stream))
+        return jk.value, xc.value
+
     def set_timing(self, on: bool = True):
         _lib.check(self.lib.dftb_plan_set_timing(self.h, 1 if on else 0))
 

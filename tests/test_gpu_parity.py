@@ -263,3 +263,22 @@ def test_roothaan_device(gpu_lib, sto3g, golden, golden_arrays):
         ref = golden_arrays[f"{name}_core_eps"]
         s = solve_roothaan(golden_arrays[f"{name}_V"] + golden_arrays[f"{name}_T"], golden_arrays[f"{name}_S"])
         np.testing.assert_allclose(s.epsilon, ref, atol=1e-10)
+
+
+def test_kernel_times_leave_results_unchanged(gpu_lib, sto3g):
+    """dftb_plan_kernel_times re-runs J/K and XC for the bench rooflines without touching results."""
+    from paper_2311_01135_b200 import synth
+    from paper_2311_01135_b200.engine import Plan
+
+    mols = synth.batch(6, 4, seed=5)
+    opts = SCFOptions(max_iterations=6, convergence_std=0.0, grid_level=0, precision="f32")
+    with Plan(mols, sto3g, opts.engine()) as p:
+        p.run()
+        before = p.fetch(want_C=False)
+        jk, xc = p.kernel_times(2)
+        after = p.fetch(want_C=False)
+        assert jk > 0.0 and xc > 0.0
+        np.testing.assert_array_equal(before.E_total, after.E_total)
+        np.testing.assert_array_equal(before.converged, after.converged)
+        p.run()                                     # a rerun still reproduces the labels
+        np.testing.assert_array_equal(p.fetch(want_C=False).E_total, before.E_total)
