@@ -195,23 +195,30 @@ __global__ void __launch_bounds__(XC_THREADS) k_xc(DevBatch b, const int *ctas) 
                     for (int a = 0; a < 4; ++a)
 #pragma unroll
                         for (int c = 0; c < 4; ++c) t[a][c] = (W)0;
-                    for (int k = 0; k < N; ++k) {
-                        W f[4], r4[4];
-                        Vec4<W>::ld(phi + swz<BP>(k, 4 * pg), f);
-                        Vec4<W>::ld(rho + k * NP + 4 * q, r4);
+                    // k ascending in groups of 4 rows: the swizzled column of a 4-row group is
+                    // one XOR (rows >= N are zero in phi and rho, so the tail adds exact zeros)
+                    for (int kq = 0; kq < (N + 3) / 4; ++kq) {
+                        const W *pr = phi + 4 * kq * BP + (((pg ^ kq) & (BP / 4 - 1)) << 2);
+                        const W *rr = rho + 4 * kq * NP + 4 * q;
 #pragma unroll
-                        for (int a = 0; a < 4; ++a)
+                        for (int r = 0; r < 4; ++r) {
+                            W f[4], r4[4];
+                            Vec4<W>::ld(pr + r * BP, f);
+                            Vec4<W>::ld(rr + r * NP, r4);
 #pragma unroll
-                            for (int c = 0; c < 4; ++c) t[a][c] += f[a] * r4[c];
+                            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                                for (int c = 0; c < 4; ++c) t[a][c] += f[a] * r4[c];
+                        }
                     }
+                    const int qo = 4 * q * BP + (((pg ^ q) & (BP / 4 - 1)) << 2);   // rows 4q..4q+3
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
-                        const int nu = 4 * q + c;
                         W f0[4], f1[4], f2[4], f3[4];
-                        Vec4<W>::ld(phi + swz<BP>(nu, 4 * pg), f0);
-                        Vec4<W>::ld(phi + PL + swz<BP>(nu, 4 * pg), f1);
-                        Vec4<W>::ld(phi + 2 * PL + swz<BP>(nu, 4 * pg), f2);
-                        Vec4<W>::ld(phi + 3 * PL + swz<BP>(nu, 4 * pg), f3);
+                        Vec4<W>::ld(phi + qo + c * BP, f0);
+                        Vec4<W>::ld(phi + PL + qo + c * BP, f1);
+                        Vec4<W>::ld(phi + 2 * PL + qo + c * BP, f2);
+                        Vec4<W>::ld(phi + 3 * PL + qo + c * BP, f3);
 #pragma unroll
                         for (int a = 0; a < 4; ++a) {
                             n4[a] += t[a][c] * f0[a];
@@ -298,12 +305,14 @@ __global__ void __launch_bounds__(XC_THREADS) k_xc(DevBatch b, const int *ctas) 
             const int T = tid + j * XC_THREADS;
             if (T < NT) {
                 const int qa = T / NQ, qb = T % NQ;
-                for (int p4 = 0; p4 < BP; p4 += 4) {
+                const W *pa = phi + 4 * qa * BP, *pb = wv + 4 * qb * BP;   // rows 4qa.., 4qb..
+                for (int c4 = 0; c4 < BP / 4; ++c4) {
+                    const int ca = ((c4 ^ qa) & (BP / 4 - 1)) << 2, cb = ((c4 ^ qb) & (BP / 4 - 1)) << 2;
                     W fa[4][4], fb[4][4];
 #pragma unroll
                     for (int a = 0; a < 4; ++a) {
-                        Vec4<W>::ld(phi + swz<BP>(4 * qa + a, p4), fa[a]);
-                        Vec4<W>::ld(wv + swz<BP>(4 * qb + a, p4), fb[a]);
+                        Vec4<W>::ld(pa + a * BP + ca, fa[a]);
+                        Vec4<W>::ld(pb + a * BP + cb, fb[a]);
                     }
 #pragma unroll
                     for (int a = 0; a < 4; ++a)
