@@ -64,7 +64,8 @@ struct XCL {
     static constexpr size_t dn = pt + sizeof(double) * 4 * BP;
     static constexpr size_t red = dn + sizeof(double) * 4 * BP;
     static constexpr size_t fpt = red + sizeof(double) * 32;      // functional parts [10][BP]
-    static constexpr size_t shd = fpt + sizeof(double) * 10 * BP;
+    static constexpr size_t dw = fpt + sizeof(double) * 10 * BP;  // wv coefficients [4][BP] (W)
+    static constexpr size_t shd = dw + ((sizeof(W) * 4 * BP + 15) & ~(size_t)15);
     static size_t bytes(int nsh) { return shd + sizeof(double) * XC_SHD * (size_t)nsh; }
 };
 
@@ -140,6 +141,7 @@ __global__ void __launch_bounds__(XC_THREADS) k_xc(DevBatch b, const int *ctas) 
     double *dn = (double *)(xsm + L::dn);
     double *red = (double *)(xsm + L::red);
     double *fpt = (double *)(xsm + L::fpt);
+    W *dw = (W *)(xsm + L::dw);
     double *shd = (double *)(xsm + L::shd);
     const int tid = threadIdx.x;
     const double *rg = b.rho + b.m_mat0[m];
@@ -283,21 +285,21 @@ __global__ void __launch_bounds__(XC_THREADS) k_xc(DevBatch b, const int *ctas) 
                 const double ww = (double)(W)w;
                 const double a = (double)(W)(0.5 * ww * (double)(W)o.vrho);
                 const double bb = (double)(W)(2.0 * ww * (double)(W)o.vsigma);
-                d[0] = a;
-                d[1] = bb * gx;
-                d[2] = bb * gy;
-                d[3] = bb * gz;
+                dw[pt_i] = (W)a;
+                dw[BP + pt_i] = (W)(bb * gx);
+                dw[2 * BP + pt_i] = (W)(bb * gy);
+                dw[3 * BP + pt_i] = (W)(bb * gz);
             } else {
-                d[0] = d[1] = d[2] = d[3] = 0.0;
+                dw[pt_i] = dw[BP + pt_i] = dw[2 * BP + pt_i] = dw[3 * BP + pt_i] = (W)0;
             }
             }
         }
         __syncthreads();
         for (int t = tid; t < PL; t += XC_THREADS) {       // ---- wv = a phi + b . grad phi
             const int row = t / BP, p = t % BP;
-            const double *d = dn + 4 * p;
             const int o = swz<BP>(row, p);
-            wv[o] = (W)d[0] * phi[o] + (W)d[1] * phi[PL + o] + (W)d[2] * phi[2 * PL + o] + (W)d[3] * phi[3 * PL + o];
+            wv[o] = dw[p] * phi[o] + dw[BP + p] * phi[PL + o] + dw[2 * BP + p] * phi[2 * PL + o] +
+                    dw[3 * BP + p] * phi[3 * PL + o];
         }
         __syncthreads();
 #pragma unroll
