@@ -282,3 +282,23 @@ def test_kernel_times_leave_results_unchanged(gpu_lib, sto3g):
         np.testing.assert_array_equal(before.converged, after.converged)
         p.run()                                     # a rerun still reproduces the labels
         np.testing.assert_array_equal(p.fetch(want_C=False).E_total, before.E_total)
+
+
+@pytest.mark.slow
+def test_largest_buckets_against_oracle(gpu_lib, sto3g, oracle):
+    """N_ao 84-94 (14 heavy atoms): the NB = 96 J/K bucket (f64: two-row chunks, one stage
+    buffer) and the NQ = 24 XC bucket, f64 SCF vs the CPU oracle and f32 within tolerance."""
+    from paper_2311_01135_b200 import synth
+
+    mols = synth.batch(2, 14, seed=3)
+    opts = dict(max_iterations=8, convergence_std=0.0, grid_level=0)
+    dev64 = scf_batch(mols, sto3g, SCFOptions(precision="f64", **opts))
+    dev32 = scf_batch(mols, sto3g, SCFOptions(precision="f32", **opts))
+    for m, r64, r32 in zip(mols, dev64, dev32):
+        assert r64.n_ao > 80
+        ref = oracle.scf(oracle.Mol(tuple(m.atomic_numbers), np.asarray(m.positions)), "f64",
+                         opts["max_iterations"], 0.0, opts["grid_level"])
+        assert abs(r64.E_total - ref.E_total) < 1e-7
+        np.testing.assert_allclose(r64.energy_history, ref.history, rtol=0, atol=1e-7)
+        np.testing.assert_allclose(np.asarray(r64.solution.epsilon), ref.epsilon, rtol=0, atol=1e-7)
+        assert abs(r32.E_total - ref.E_total) < 2e-3
