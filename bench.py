@@ -349,6 +349,8 @@ def run_ours(args, ws, rank, local):
     jk_gbs = info["eri_bytes"] / (ms_jk / 1000.0) / 1e9
     hbm_peak, hbm_src = _hbm_peak()
     n_ao_mean = float(np.mean(plan.pk.mol_nao))
+    npp_m = nao * (nao + 1) / 2
+    n_ao_ints = float(np.sum(npp_m * (npp_m + 1) / 2))
     mol_nao_sq = int(sum(int(x) ** 2 for x in plan.pk.mol_nao))
     for p_ in plans:
         p_.close()
@@ -382,7 +384,11 @@ def run_ours(args, ws, rank, local):
                                            "scf_loop": stage[2]},
                    "stage_ms_isolated": {"setup_eri": iso_stage[0], "onee_grid_orth_guess": iso_stage[1],
                                          "scf_loop": iso_stage[2]},
-                   "eri_quartets_per_s": nq / (iso_stage[0] / 1000.0), "failed_molecules": bad},
+                   "eri_quartets_per_s": nq / (iso_stage[0] / 1000.0),
+                   "eri_ao_integrals_per_s": n_ao_ints / (iso_stage[0] / 1000.0),
+                   "eri_rates_note": "split-shell quartets surviving Schwarz / canonical (8-fold unique) AO "
+                                     "integrals of one batch over the isolated ERI-stage time",
+                   "failed_molecules": bad},
         "clocks": clocks,
         "gpu_launches": launches,
         "e2e": {"value": ws * n_res / (e2e / 1000.0), "unit": UNIT, "ms_per_step": e2e,
