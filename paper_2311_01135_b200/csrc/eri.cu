@@ -9,10 +9,14 @@
 //    slice, which is warp-uniform because it is blockIdx.y);
 //  * primitive-pair records are SoA with the pair index fastest, so the 32 lanes of
 //    a warp (consecutive ket pairs) read one coalesced 256-byte line per field;
-//  * results go to a dense, 8-fold packed AO-pair triangle per molecule,
-//    element (P, Q) with P = ij >= Q = kl at offset P(P+1)/2 + Q: exactly the
-//    reference's canonical composite order, so the J/K digestion streams rows
-//    with no index arrays and eri_packed's canonical list is a stream compaction.
+//  * results go to the dense per-molecule store in the "ket-tiled rows" layout
+//    (common.cuh): one row per canonical bra pair P = (i, j), its kets as 4x4 tiles of
+//    the symmetric ket matrix, so the J/K kernel streams whole rows with bulk copies and
+//    16-byte tile loads; every canonical element has exactly one writer, and the stores
+//    are streaming (evict-first: the store is next read by J/K, after the whole stage);
+//  * the two ket-split classes (LL|LL, LL|LS) take two ket components per slice and
+//    every class except SS|SS keeps its ket pair's nine primitive records in shared
+//    memory (they are re-read once per bra primitive).
 #include "common.cuh"
 #include "md.cuh"
 

@@ -6,8 +6,8 @@
                      then k_compact applies the reference's three screens (split-shell
                      pair bound, AO-level bound, |v| >= eps) and emits the canonical
                      list in composite order;
-  * build_jk      -> the packed list is scattered into a dense store and digested by
-                     the row-owner J/K kernel (deterministic, no atomics).
+  * build_jk      -> the packed list is scattered into the dense (ket-tiled) store and
+                     digested by the tile J/K kernel (deterministic, no atomics).
 Values are computed without the reference's primitive-pair screen, i.e. they equal
 the exact (screen_eps = 0) integrals; the *selection* follows eps exactly.
 Dense unpacking and the binary dump formats are host-side formatting, as in the
