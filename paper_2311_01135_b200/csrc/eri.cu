@@ -126,13 +126,19 @@ __device__ __forceinline__ void store_eri(ST *eri, int64_t base, int i, int j, i
 // next to the SM removes ~8/9 of the kernel's load traffic.  Slots [slot][prim][thread];
 // S-only kets need 7 fields (the screening bound goes to slot 6).
 constexpr int ERI_T = 128;
+// Seven fields are cached (p, P, 1/2p, c_ss, bound); the p-coefficient products c_sp,
+// c_ps, c_pp of L kets are read from global memory: they are consumed only after the
+// Boys / R_tuv chain, which hides their latency, and leaving them out keeps the cache at
+// 64.5 KB per CTA (3 CTAs per SM instead of 2).
 template <bool LKET>
 struct KetSmem {
-    static constexpr int NSLOT = LKET ? 10 : 7;
+    static constexpr int NSLOT = 7;
     const double *s;
     int lane;
-    __device__ __forceinline__ static int slot(int f) { return (!LKET && f == PF_BOUND) ? 6 : f; }
-    __device__ __forceinline__ double get(int f, int k, int64_t) const {
+    PPView g;
+    __device__ __forceinline__ static int slot(int f) { return f == PF_BOUND ? 6 : f; }
+    __device__ __forceinline__ double get(int f, int k, int64_t pair) const {
+        if (f == PF_CSP || f == PF_CPS || f == PF_CPP) return g.get(f, k, pair);
         return s[(slot(f) * 9 + k) * ERI_T + lane];
     }
 };
@@ -163,11 +169,11 @@ __global__ void __launch_bounds__(ERI_T) k_eri(DevBatch b, int cls, double eps, 
     const PPView V{b.pp, b.n_pair};
     extern __shared__ double eri_ksm[];
     using KS = KetSmem<(KC || KD)>;
-    const KS VK{eri_ksm, (int)threadIdx.x};
+    const KS VK{eri_ksm, (int)threadIdx.x, V};
     if constexpr (KSM) {
 #pragma unroll
         for (int f = 0; f < KS::NSLOT; ++f) {
-            const int field = (f == 6 && !(KC || KD)) ? (int)PF_BOUND : f;
+            const int field = f == 6 ? (int)PF_BOUND : f;
 #pragma unroll
             for (int k = 0; k < 9; ++k) eri_ksm[(f * 9 + k) * ERI_T + threadIdx.x] = V.get(field, k, Qp);
         }
