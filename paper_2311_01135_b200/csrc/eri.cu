@@ -126,19 +126,22 @@ __device__ __forceinline__ void store_eri(ST *eri, int64_t base, int i, int j, i
 // next to the SM removes ~8/9 of the kernel's load traffic.  Slots [slot][prim][thread];
 // S-only kets need 7 fields (the screening bound goes to slot 6).
 constexpr int ERI_T = 128;
-// Seven fields are cached (p, P, 1/2p, c_ss, bound); the p-coefficient products c_sp,
-// c_ps, c_pp of L kets are read from global memory: they are consumed only after the
-// Boys / R_tuv chain, which hides their latency, and leaving them out keeps the cache at
-// 64.5 KB per CTA (3 CTAs per SM instead of 2).
+// Only the latency-critical fields are cached (p, P, 1/2p, bound, and c_ss for L kets);
+// the coefficient products read from global memory are consumed after the Boys / R_tuv
+// chain, which hides their latency, and leaving them out keeps the cache small enough for
+// 3 (L kets, 64.5 KB) or 4 (S kets, 55 KB) CTAs per SM.
 template <bool LKET>
 struct KetSmem {
-    static constexpr int NSLOT = 7;
+    // L kets: p, P, 1/2p, c_ss, bound (7 slots); S kets: p, P, 1/2p, bound (6 slots, 55 KB
+    // per CTA: 4 CTAs per SM) with c_ss from global as well
+    static constexpr int NSLOT = LKET ? 7 : 6;
     const double *s;
     int lane;
     PPView g;
-    __device__ __forceinline__ static int slot(int f) { return f == PF_BOUND ? 6 : f; }
+    __device__ __forceinline__ static int slot(int f) { return f == PF_BOUND ? NSLOT - 1 : f; }
+    __device__ __forceinline__ static int field(int sl) { return sl == NSLOT - 1 ? (int)PF_BOUND : sl; }
     __device__ __forceinline__ double get(int f, int k, int64_t pair) const {
-        if (f == PF_CSP || f == PF_CPS || f == PF_CPP) return g.get(f, k, pair);
+        if (f == PF_CSP || f == PF_CPS || f == PF_CPP || (!LKET && f == PF_CSS)) return g.get(f, k, pair);
         return s[(slot(f) * 9 + k) * ERI_T + lane];
     }
 };
@@ -173,7 +176,7 @@ __global__ void __launch_bounds__(ERI_T) k_eri(DevBatch b, int cls, double eps, 
     if constexpr (KSM) {
 #pragma unroll
         for (int f = 0; f < KS::NSLOT; ++f) {
-            const int field = f == 6 ? (int)PF_BOUND : f;
+            const int field = KS::field(f);
 #pragma unroll
             for (int k = 0; k < 9; ++k) eri_ksm[(f * 9 + k) * ERI_T + threadIdx.x] = V.get(field, k, Qp);
         }
