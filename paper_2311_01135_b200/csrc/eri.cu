@@ -130,18 +130,18 @@ constexpr int ERI_T = 128;
 // the coefficient products read from global memory are consumed after the Boys / R_tuv
 // chain, which hides their latency, and leaving them out keeps the cache small enough for
 // 3 (L kets, 64.5 KB) or 4 (S kets, 55 KB) CTAs per SM.
-template <bool LKET>
+template <bool LKET, int NS = (LKET ? 7 : 6)>
 struct KetSmem {
-    // L kets: p, P, 1/2p, c_ss, bound (7 slots); S kets: p, P, 1/2p, bound (6 slots, 55 KB
-    // per CTA: 4 CTAs per SM) with c_ss from global as well
-    static constexpr int NSLOT = LKET ? 7 : 6;
+    // 7 slots: p, P, 1/2p, c_ss, bound; 6 slots: p, P, 1/2p, bound (55 KB per CTA: 4 CTAs
+    // per SM), c_ss from global as well
+    static constexpr int NSLOT = NS;
     const double *s;
     int lane;
     PPView g;
     __device__ __forceinline__ static int slot(int f) { return f == PF_BOUND ? NSLOT - 1 : f; }
     __device__ __forceinline__ static int field(int sl) { return sl == NSLOT - 1 ? (int)PF_BOUND : sl; }
     __device__ __forceinline__ double get(int f, int k, int64_t pair) const {
-        if (f == PF_CSP || f == PF_CPS || f == PF_CPP || (!LKET && f == PF_CSS)) return g.get(f, k, pair);
+        if (f == PF_CSP || f == PF_CPS || f == PF_CPP || (NS == 6 && f == PF_CSS)) return g.get(f, k, pair);
         return s[(slot(f) * 9 + k) * ERI_T + lane];
     }
 };
@@ -151,8 +151,9 @@ struct KetSmem {
 // R_tuv of all 81 primitive quartets, so fewer slices trade registers for less recomputation.
 // KSM: keep the ket records in shared memory (off for SS|SS, whose occupancy it would cut
 // from 9 to 3 CTAs per SM for a class that is cheap per primitive quartet)
-template <int KA, int KB, int KC, int KD, int KPS, typename ST, bool KSM = true>
-__global__ void __launch_bounds__(ERI_T) k_eri(DevBatch b, int cls, double eps, double prim_cut, ST *eri) {
+template <int KA, int KB, int KC, int KD, int KPS, typename ST, bool KSM = true, int MINB = 1,
+          int NS = ((KC || KD) ? 7 : 6)>
+__global__ void __launch_bounds__(ERI_T, MINB) k_eri(DevBatch b, int cls, double eps, double prim_cut, ST *eri) {
     constexpr int NA = KA ? 4 : 1, NB = KB ? 4 : 1, NC = KC ? 4 : 1, ND = KD ? 4 : 1;
     constexpr int NKET = NC * ND, NKS = KPS ? KPS : NKET, NSL = NKET / NKS;
     static_assert(NKET % NKS == 0, "slice size must divide the ket component count");
@@ -171,8 +172,7 @@ __global__ void __launch_bounds__(ERI_T) k_eri(DevBatch b, int cls, double eps, 
     load_geo(b, Qp, C, D);
     const PPView V{b.pp, b.n_pair};
     extern __shared__ double eri_ksm[];
-    using KS = KetSmem<(KC || KD)>;
-    const KS VK{eri_ksm, (int)threadIdx.x, V};
+    using KS = KetSmem<(KC || KD), NS>;
     if constexpr (KSM) {
 #pragma unroll
         for (int f = 0; f < KS::NSLOT; ++f) {
@@ -191,8 +191,12 @@ __global__ void __launch_bounds__(ERI_T) k_eri(DevBatch b, int cls, double eps, 
         for (int x = 0; x < NA * NB; ++x)
 #pragma unroll
             for (int y = 0; y < NKS; ++y) out[x][y] = 0.0;
-        if constexpr (KSM) eri_quartet_kv<KA, KB, KC, KD, KC0, NKS>(V, VK, Pp, Qp, A, B, C, D, b.boys, prim_cut, out);
-        else eri_quartet_kv<KA, KB, KC, KD, KC0, NKS>(V, V, Pp, Qp, A, B, C, D, b.boys, prim_cut, out);
+        if constexpr (KSM) {
+            const KS VK{eri_ksm, (int)threadIdx.x, V};
+            eri_quartet_kv<KA, KB, KC, KD, KC0, NKS>(V, VK, Pp, Qp, A, B, C, D, b.boys, prim_cut, out);
+        } else {
+            eri_quartet_kv<KA, KB, KC, KD, KC0, NKS>(V, V, Pp, Qp, A, B, C, D, b.boys, prim_cut, out);
+        }
         // single writer per canonical element: for a diagonal shell pair only the
         // (i >= j) component writes, for a diagonal quartet only the (ij >= kl) image
         const bool dab = b.p_sa[Pp] == b.p_sb[Pp], dcd = b.p_sa[Qp] == b.p_sb[Qp], dpq = Pp == Qp;
@@ -281,18 +285,28 @@ void launch_schwarz(const DevBatch &b, const int64_t *host_totals, cudaStream_t 
     if (b.n_pair) k_pair_q<<<nblk(b.n_pair, 128), 128, 0, s>>>(b);
 }
 
-template <int KA, int KB, int KC, int KD, int KPS, bool KSM = true, typename ST>
+template <int KA, int KB, int KC, int KD, int KPS, bool KSM = true, int MINB = 1, int NS = ((KC || KD) ? 7 : 6),
+          typename ST>
 static void launch_cls(const DevBatch &b, int cls, int64_t n, double eps, double prim_cut, ST *eri,
                        cudaStream_t s, int *nlaunch) {
     if (!n) return;
     constexpr int NKET = (KC ? 4 : 1) * (KD ? 4 : 1), NSL = NKET / (KPS ? KPS : NKET);
-    const size_t sm = KSM ? sizeof(double) * KetSmem<(KC || KD)>::NSLOT * 9 * ERI_T : 0;
-    auto kern = k_eri<KA, KB, KC, KD, KPS, ST, KSM>;
+    const size_t sm = KSM ? sizeof(double) * KetSmem<(KC || KD), NS>::NSLOT * 9 * ERI_T : 0;
+    auto kern = k_eri<KA, KB, KC, KD, KPS, ST, KSM, MINB, NS>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     kern<<<dim3(nblk(n, ERI_T), NSL), ERI_T, sm, s>>>(b, cls, eps, prim_cut, eri);
     ++*nlaunch;
 }
 
+#ifndef ERI_S_MINB
+#define ERI_S_MINB 4       // LL|SS, LS|SS: 4 CTAs per SM (55 KB ket cache, <= 128 registers)
+#endif
+#ifndef ERI_LSLS_MINB
+#define ERI_LSLS_MINB 4    // LS|LS: 4 CTAs per SM (<= 128 registers, 6-slot ket cache)
+#endif
+#ifndef ERI_LSLS_NS
+#define ERI_LSLS_NS 6
+#endif
 #ifndef ERI_KPS_LL
 #define ERI_KPS_LL 2       // LL|LL: 8 slices of 2 ket components
 #endif
@@ -305,9 +319,9 @@ static void launch_eri_t(const DevBatch &b, const int64_t *tot, double eps, doub
                          ST *eri, cudaStream_t s, int *nlaunch) {
     launch_cls<1, 1, 1, 1, ERI_KPS_LL>(b, 0, tot[0], eps, prim_cut, eri, s, nlaunch);
     launch_cls<1, 1, 1, 0, ERI_KPS_LS>(b, 1, tot[1], eps, prim_cut, eri, s, nlaunch);
-    launch_cls<1, 1, 0, 0, 0>(b, 2, tot[2], eps, prim_cut, eri, s, nlaunch);
-    launch_cls<1, 0, 1, 0, 0>(b, 3, tot[3], eps, prim_cut, eri, s, nlaunch);
-    launch_cls<1, 0, 0, 0, 0>(b, 4, tot[4], eps, prim_cut, eri, s, nlaunch);
+    launch_cls<1, 1, 0, 0, 0, true, ERI_S_MINB>(b, 2, tot[2], eps, prim_cut, eri, s, nlaunch);
+    launch_cls<1, 0, 1, 0, 0, true, ERI_LSLS_MINB, ERI_LSLS_NS>(b, 3, tot[3], eps, prim_cut, eri, s, nlaunch);
+    launch_cls<1, 0, 0, 0, 0, true, ERI_S_MINB>(b, 4, tot[4], eps, prim_cut, eri, s, nlaunch);
     launch_cls<0, 0, 0, 0, 0, false>(b, 5, tot[5], eps, prim_cut, eri, s, nlaunch);
 }
 
