@@ -302,3 +302,20 @@ def test_largest_buckets_against_oracle(gpu_lib, sto3g, oracle):
         np.testing.assert_allclose(r64.energy_history, ref.history, rtol=0, atol=1e-7)
         np.testing.assert_allclose(np.asarray(r64.solution.epsilon), ref.epsilon, rtol=0, atol=1e-7)
         assert abs(r32.E_total - ref.E_total) < 2e-3
+
+
+@pytest.mark.slow
+def test_config5_shape_level3_convergence(gpu_lib, sto3g):
+    """configs[4]-shaped run (11 heavy atoms, f64, grid level 3, convergence 1e-9, max 50) on
+    four molecules: the large-grid XC path (hundreds of CTAs per molecule) converges, and a
+    molecule's labels do not depend on the batch it runs in."""
+    from paper_2311_01135_b200 import synth
+
+    mols = synth.batch(4, 11, seed=11)
+    opts = SCFOptions(precision="f64", grid_level=3, convergence_std=1e-9, max_iterations=50)
+    batch = scf_batch(mols, sto3g, opts)
+    alone = scf_batch(mols[2:3], sto3g, opts)[0]
+    for r in batch:
+        assert r.converged and r.iterations <= 50
+        assert np.std(r.energy_history[-5:]) < 1e-9
+    assert alone.E_total == batch[2].E_total and alone.iterations == batch[2].iterations
