@@ -54,7 +54,8 @@ HD int64_t eri_size(int N) { return eri_slab0(N); }
 // "local" = within one molecule.
 struct DevBatch {
     int n_mol, n_atom, n_shell, n_pair, n_pts;
-    int prec;                 // 0 f64, 1 f32 (ERI store + XC arithmetic)
+    int prec;                 // 0 f64, 1 f32 (ERI values + XC arithmetic)
+    int eri64;                // ERI store element type: 1 = f64 (f32 build: f32-rounded values)
     // molecules
     const int *m_nao, *m_nocc, *m_natom, *m_atom0, *m_nshell, *m_shell0, *m_pair0;
     const int *m_npl;         // [n_mol*3] pair counts LL, LS, SS

@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(ERI_T, MINB) k_eri(DevBatch b, int cls, double
                 if (dab && i < j) continue;
                 if (dcd && k < l) continue;
                 if (dpq && pidx(i, j) < pidx(k, l)) continue;
-                store_eri(eri, base, i, j, k, l, out[x][y]);
+                store_eri(eri, base, i, j, k, l, b.prec ? (double)(float)out[x][y] : out[x][y]);
             }
     });
 }
@@ -327,7 +327,7 @@ static void launch_eri_t(const DevBatch &b, const int64_t *tot, double eps, doub
 
 void launch_eri(const DevBatch &b, const int64_t *tot, double eps, double prim_cut, cudaStream_t s,
                 int *nlaunch) {
-    if (b.prec == 0) launch_eri_t<double>(b, tot, eps, prim_cut, (double *)b.eri, s, nlaunch);
+    if (b.eri64) launch_eri_t<double>(b, tot, eps, prim_cut, (double *)b.eri, s, nlaunch);
     else launch_eri_t<float>(b, tot, eps, prim_cut, (float *)b.eri, s, nlaunch);
 }
 

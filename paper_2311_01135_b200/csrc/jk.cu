@@ -380,7 +380,7 @@ static void launch_jk_t(const DevBatch &b, const int *bucket_ctas, const int *bu
 // bucket_ctas: device array of CTA indices grouped by AO-count bucket; bucket_n: host counts [6]
 int launch_jk(const DevBatch &b, const int *bucket_ctas, const int *bucket_n, cudaStream_t s) {
     if (b.n_jk_cta == 0) return 0;
-    if (b.prec == 0) launch_jk_t<double>(b, bucket_ctas, bucket_n, s);
+    if (b.eri64) launch_jk_t<double>(b, bucket_ctas, bucket_n, s);
     else launch_jk_t<float>(b, bucket_ctas, bucket_n, s);
     int k = 0;
     for (int i = 0; i < 6; ++i) k += bucket_n[i] > 0;

@@ -128,14 +128,14 @@ static int mol_npp(const DevBatch &b, int mol) {
 
 void launch_compact_count(const DevBatch &b, int mol, double eps, const double *qsp, int64_t *rowcnt, cudaStream_t s) {
     const int npp = mol_npp(b, mol);
-    if (b.prec == 0) k_compact<double><<<npp, 128, 0, s>>>(b, mol, eps, qsp, rowcnt, nullptr, 0, 0, 0, 0, 0);
+    if (b.eri64) k_compact<double><<<npp, 128, 0, s>>>(b, mol, eps, qsp, rowcnt, nullptr, 0, 0, 0, 0, 0);
     else k_compact<float><<<npp, 128, 0, s>>>(b, mol, eps, qsp, rowcnt, nullptr, 0, 0, 0, 0, 0);
 }
 
 void launch_compact_write(const DevBatch &b, int mol, double eps, const double *qsp, const int64_t *rowoff,
                           uint16_t *oi, uint16_t *oj, uint16_t *ok, uint16_t *ol, double *ov, cudaStream_t s) {
     const int npp = mol_npp(b, mol);
-    if (b.prec == 0) k_compact<double><<<npp, 128, 0, s>>>(b, mol, eps, qsp, nullptr, rowoff, oi, oj, ok, ol, ov);
+    if (b.eri64) k_compact<double><<<npp, 128, 0, s>>>(b, mol, eps, qsp, nullptr, rowoff, oi, oj, ok, ol, ov);
     else k_compact<float><<<npp, 128, 0, s>>>(b, mol, eps, qsp, nullptr, rowoff, oi, oj, ok, ol, ov);
 }
 

@@ -53,7 +53,10 @@ static int fail(int code, const std::string &msg) {
     } while (0)
 
 static constexpr int XC_CHUNK = 2048;
-static constexpr int JK_SPLIT = 12;     // target J/K CTAs per molecule (largest slab permitting)
+static constexpr int JK_SPLIT = 12;
+#ifndef ERI64_F32
+#define ERI64_F32 0     // f32 build: keep the (f32-rounded) ERI store in f64 (no f32->f64 in J/K)
+#endif     // target J/K CTAs per molecule (largest slab permitting)
 
 struct dftb_plan {
     DevBatch d{};
@@ -389,7 +392,8 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
     const size_t o_dbg = L.add<long long>((size_t)nm * 16);
     size_t o_ints[7];
     for (int k = 0; k < 7; ++k) o_ints[k] = L.add<int>(nm);
-    const int esz = opts->precision ? 4 : 8;
+    const int eri64 = !opts->precision || ERI64_F32;
+    const int esz = eri64 ? 8 : 4;
     p->eri_off = L.add<char>((size_t)eri0[nm] * esz);
     p->eri_bytes = (size_t)eri0[nm] * esz;
     p->mem_bytes = (L.off + 255) & ~(size_t)255;
@@ -434,6 +438,7 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
 #define PTR(T, o) reinterpret_cast<T *>(M + (o))
     d.n_mol = nm; d.n_atom = in->n_atom; d.n_shell = in->n_shell; d.n_pair = npair; d.n_pts = (int)npts_tot;
     d.prec = opts->precision ? 1 : 0;
+    d.eri64 = eri64;
     d.m_nao = PTR(int, o_m_nao); d.m_nocc = PTR(int, o_m_nocc); d.m_natom = PTR(int, o_m_natom);
     d.m_atom0 = PTR(int, o_m_atom0); d.m_nshell = PTR(int, o_m_nshell); d.m_shell0 = PTR(int, o_m_shell0);
     d.m_pair0 = PTR(int, o_m_pair0); d.m_npl = PTR(int, o_m_npl);
@@ -596,7 +601,7 @@ int dftb_plan_eri_load(dftb_plan *p, int32_t mol, int64_t count, const uint16_t 
     if (!p || mol < 0 || mol >= p->d.n_mol) return fail(DFTB_EINVAL, "bad arguments");
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t npp = p->npp0[mol + 1] - p->npp0[mol];
-    const int esz = p->d.prec ? 4 : 8;
+    const int esz = p->d.eri64 ? 8 : 4;
     const int N = p->nao[mol];
     const int64_t n = eri_size(N);
     const int64_t e0 = p->eri0[mol];
@@ -604,7 +609,7 @@ int dftb_plan_eri_load(dftb_plan *p, int32_t mol, int64_t count, const uint16_t 
     for (int64_t e = 0; e < count; ++e) {
         if (i[e] >= N || j[e] >= N || k[e] >= N || l[e] >= N) return fail(DFTB_EINVAL, "index out of range for n_ao");
         const int64_t off = eri_pos(i[e], j[e], k[e], l[e]);
-        if (esz == 8) reinterpret_cast<double *>(host.data())[off] = v[e];
+        if (esz == 8) reinterpret_cast<double *>(host.data())[off] = p->d.prec ? (double)(float)v[e] : v[e];
         else reinterpret_cast<float *>(host.data())[off] = (float)v[e];
     }
     CK(cudaMemcpyAsync(p->mem + p->eri_off + (size_t)e0 * esz, host.data(), host.size(), cudaMemcpyHostToDevice, st));
@@ -862,7 +867,7 @@ int dftb_plan_get(dftb_plan *p, const char *which, int32_t mol, double *host, in
     else if (w == "eri") {
         // returned unpadded, in canonical composite order (row P, Q <= P)
         const int64_t npp = p->npp0[mol + 1] - p->npp0[mol];
-        const int esz = d.prec ? 4 : 8;
+        const int esz = d.eri64 ? 8 : 4;
         const int N = p->nao[mol];
         cnt = npp * (npp + 1) / 2;
         if (n < cnt) return fail(DFTB_EINVAL, "host buffer too small");
