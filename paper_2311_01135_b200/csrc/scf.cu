@@ -19,11 +19,10 @@ constexpr int GST = (KP * NMAX + 255) / 256;   // staging elements per thread pe
 
 struct Arena {
     int nm;             // arena dimension (largest N of the batch) and staging leading dim
-    double *A, *B, *W;  // nm*nm each (W >= 2*KP*nm); W doubles as GEMM staging and Jacobi's 2nd A
-    double *sa, *sb;    // KP*nm each, inside W
-    double *cs, *sn;    // rotations, double-buffered [2][NPH]
+    double *A, *B;      // nm*nm each (B >= 2*KP*64): Jacobi's matrix and eigenvectors
+    double *sa, *sb;    // GEMM staging [KP][64] each, inside B (no GEMM reads or writes B)
+    double *cs, *sn;    // rotations of the current step [NPH] (2*NPH allocated)
     int *pp, *qq;       // rotation pairs [2][NPH]
-    int *pos;           // index -> 2*pair + is_q, [2][NMAX+2]
     int *perm;          // [NMAX]
     double *dv;         // [NMAX]
     double *Bs;         // [10*10] DIIS system
@@ -34,17 +33,16 @@ struct Arena {
 
 constexpr int NPH = NMAX / 2 + 1;
 
-HD size_t arena_w(int nm) { return (size_t)(nm * nm > 2 * KP * 64 ? nm * nm : 2 * KP * 64); }
+HD size_t arena_b(int nm) { return (size_t)(nm * nm > 2 * KP * 64 ? nm * nm : 2 * KP * 64); }
 
 __device__ __forceinline__ Arena carve(unsigned char *base, int nm) {
     Arena a;
     a.nm = nm;
     double *p = (double *)base;
     a.A = p; p += nm * nm;
-    a.B = p; p += nm * nm;
-    a.W = p; p += arena_w(nm);
-    a.sa = a.W;
-    a.sb = a.W + KP * 64;
+    a.B = p; p += arena_b(nm);
+    a.sa = a.B;
+    a.sb = a.B + KP * 64;
     a.cs = p; p += 2 * NPH;
     a.sn = p; p += 2 * NPH;
     a.dv = p; p += NMAX;
@@ -55,14 +53,13 @@ __device__ __forceinline__ Arena carve(unsigned char *base, int nm) {
     int *q = (int *)p;
     a.pp = q; q += 2 * NPH;
     a.qq = q; q += 2 * NPH;
-    a.pos = q; q += 2 * (NMAX + 2);
     a.perm = q; q += NMAX;
     return a;
 }
 
 size_t scf_smem_bytes(int nm) {
-    return sizeof(double) * (2 * (size_t)nm * nm + arena_w(nm) + 4 * NPH + NMAX + 100 + 10 + 32 + 16) +
-           sizeof(int) * (4 * NPH + 2 * (NMAX + 2) + NMAX);
+    return sizeof(double) * ((size_t)nm * nm + arena_b(nm) + 4 * NPH + NMAX + 100 + 10 + 32 + 16) +
+           sizeof(int) * (4 * NPH + NMAX);
 }
 
 // C (M x N, ldc) = alpha * op(A) op(B) + beta * C ; op(A) is M x K, op(B) is K x N.
@@ -148,11 +145,13 @@ __device__ void cta_gemm(double *C, int ldc, const double *A, int lda, bool tA, 
 }
 
 // Cyclic Jacobi, round-robin (circle) pairing: n/2 disjoint rotations per step,
-// applied at once as J^T A J on 2x2 blocks (rows of pair k1 x columns of pair k2)
-// from buffer `cur` into buffer `nxt`, V <- V J in place.  The angles of step r+1
-// are computed in the SAME pass from cur and the step-r rotations (each needs only
-// three transformed elements), so a step costs one CTA barrier.
-// Returns the buffer holding the converged (diagonal) matrix; *nsweeps = sweeps.
+// applied at once as J^T A J on 2x2 blocks (rows of pair k1 x columns of pair k2), in
+// place: the blocks partition A, so every element is read and written by exactly one
+// task.  V <- V J in place.  A step is two CTA phases: the pair owners compute the step's
+// angles from A, then every thread applies them.  In-place A (instead of a second
+// buffer) keeps the arena at two n x n matrices, which fits two post CTAs per SM for the
+// benchmark's AO counts (N <= 80) instead of one.
+// Returns A (diagonal on exit); *nsweeps = sweeps.
 constexpr int JAC_MAXT = (NPH * NPH + NMAX * NPH + SCF_THREADS - 1) / SCF_THREADS;
 
 __device__ __forceinline__ void jac_pair(int k, int r, int n2, int &p, int &q) {
@@ -172,42 +171,28 @@ __device__ __forceinline__ void jac_angle(double app, double aqq, double apq, do
     }
 }
 
-__device__ double *cta_jacobi(double *A0, double *A1, double *V, int n, const Arena &ar, int *nsweeps,
+__device__ double *cta_jacobi(double *A, double *V, int n, const Arena &ar, int *nsweeps,
                               int max_sweeps = 30, double tol = 1e-13) {
     const int tid = threadIdx.x, nt = SCF_THREADS;
     const int n2 = n + (n & 1), np = n2 / 2, R = n2 - 1;
     const int nblk = np * np, ntask = nblk + n * np;
-    int task[JAC_MAXT];
-#pragma unroll
-    for (int s = 0; s < JAC_MAXT; ++s) {
-        const int t = tid + s * nt;
-        if (t < nblk) task[s] = ((t / np) << 16) | (t % np);
-        else if (t < ntask) task[s] = (((t - nblk) / np) << 16) | ((t - nblk) % np);
-        else task[s] = -1;
-    }
-    double *cur = A0, *nxt = A1;
+    // task t -> (u, v) = divmod(t', np) by a multiply-high (exact for t' < 2^32 / np; np = 1
+    // would need 2^32, so that case is special-cased)
+    const unsigned inv_np = np > 1 ? (unsigned)((0x100000000ull + np - 1) / np) : 0u;
     const int kr = tid;
     const bool rot_owner = tid < np;
-    // rotations of global step 0 from cur directly (buffer 0)
-    if (rot_owner) {
-        int p, q;
-        jac_pair(kr, 0, n2, p, q);
-        double c = 1.0, sn = 0.0;
-        if (q < n) jac_angle(cur[p * n + p], cur[q * n + q], cur[p * n + q], c, sn);
-        ar.cs[kr] = c; ar.sn[kr] = sn; ar.pp[kr] = p; ar.qq[kr] = q;
-        ar.pos[p] = 2 * kr; ar.pos[q] = 2 * kr + 1;
-    }
-    __syncthreads();
+    const double *cs = ar.cs, *sn = ar.sn;
+    const int *pp = ar.pp, *qq = ar.qq;
     int sweeps = 0;
     for (int g = 0;; ++g) {
-        const int r = g % R, bf = g & 1, nb = bf ^ 1;
+        const int r = g % R;
         if (r == 0) {
             double off = 0.0, dg = 0.0;
             for (int t = tid; t < n * n; t += nt) {
                 const int p = t / n, q = t - p * n;
-                const double a = fabs(cur[t]);
+                const double a = fabs(A[t]);
                 if (q > p) {
-                    if (a > 1e-15 * sqrt(fabs(cur[p * n + p] * cur[q * n + q]))) off = fmax(off, a);
+                    if (a > 1e-15 * sqrt(fabs(A[p * n + p] * A[q * n + q]))) off = fmax(off, a);
                 } else if (q == p) {
                     dg = fmax(dg, a);
                 }
@@ -217,53 +202,34 @@ __device__ double *cta_jacobi(double *A0, double *A1, double *V, int n, const Ar
             if (off <= tol * dg || off < 1e-300 || sweeps >= max_sweeps) break;
             ++sweeps;
         }
-        const double *cs = ar.cs + bf * NPH, *sn = ar.sn + bf * NPH;
-        const int *pp = ar.pp + bf * NPH, *qq = ar.qq + bf * NPH, *pos = ar.pos + bf * (NMAX + 2);
-        if (rot_owner) {  // angles for step g+1 from cur and this step's rotations
-            const int r1 = (g + 1) % R;
+        if (rot_owner) {   // this step's angles from the current A
             int p, q;
-            jac_pair(kr, r1, n2, p, q);
+            jac_pair(kr, r, n2, p, q);
             double c = 1.0, s1 = 0.0;
-            if (q < n) {
-                // element (x, y) of J^T cur J
-                auto el = [&](int x, int y) {
-                    const int kx = pos[x] >> 1, ky = pos[y] >> 1;
-                    const double cx = cs[kx], sx = sn[kx], cy = cs[ky], sy = sn[ky];
-                    const int px = pp[kx], qx = qq[kx], py = pp[ky], qy = qq[ky];
-                    const double la = (pos[x] & 1) ? sx : cx, lb = (pos[x] & 1) ? cx : -sx;
-                    const double ra = (pos[y] & 1) ? sy : cy, rb = (pos[y] & 1) ? cy : -sy;
-                    const bool hx = qx < n && lb != 0.0, hy = qy < n && rb != 0.0;
-                    double v = la * ra * cur[px * n + py];
-                    if (hy) v += la * rb * cur[px * n + qy];
-                    if (hx) v += lb * ra * cur[qx * n + py];
-                    if (hx && hy) v += lb * rb * cur[qx * n + qy];
-                    return v;
-                };
-                jac_angle(el(p, p), el(q, q), el(p, q), c, s1);
-            }
-            ar.cs[nb * NPH + kr] = c; ar.sn[nb * NPH + kr] = s1;
-            ar.pp[nb * NPH + kr] = p; ar.qq[nb * NPH + kr] = q;
-            ar.pos[nb * (NMAX + 2) + p] = 2 * kr; ar.pos[nb * (NMAX + 2) + q] = 2 * kr + 1;
+            if (q < n) jac_angle(A[p * n + p], A[q * n + q], A[p * n + q], c, s1);
+            ar.cs[kr] = c; ar.sn[kr] = s1; ar.pp[kr] = p; ar.qq[kr] = q;
         }
-#pragma unroll
+        __syncthreads();
+#pragma unroll 4
         for (int s = 0; s < JAC_MAXT; ++s) {
             const int t = tid + s * nt;
             if (t >= ntask) break;
-            const int u = task[s] >> 16, v = task[s] & 0xffff;
+            const int tt = t < nblk ? t : t - nblk;
+            const int u = np > 1 ? (int)__umulhi((unsigned)tt, inv_np) : tt, v = tt - u * np;
             if (t < nblk) {
                 const double s1 = sn[u], s2 = sn[v], c1 = cs[u], c2 = cs[v];
                 const int p1 = pp[u], q1 = qq[u], p2 = pp[v], q2 = qq[v];
                 const bool hq1 = q1 < n, hq2 = q2 < n;
-                const double xpp = cur[p1 * n + p2];
-                const double xpq = hq2 ? cur[p1 * n + q2] : 0.0;
-                const double xqp = hq1 ? cur[q1 * n + p2] : 0.0;
-                const double xqq = (hq1 && hq2) ? cur[q1 * n + q2] : 0.0;
+                const double xpp = A[p1 * n + p2];
+                const double xpq = hq2 ? A[p1 * n + q2] : 0.0;
+                const double xqp = hq1 ? A[q1 * n + p2] : 0.0;
+                const double xqq = (hq1 && hq2) ? A[q1 * n + q2] : 0.0;
                 const double ypp = c1 * xpp - s1 * xqp, yqp = s1 * xpp + c1 * xqp;
                 const double ypq = c1 * xpq - s1 * xqq, yqq = s1 * xpq + c1 * xqq;
-                nxt[p1 * n + p2] = c2 * ypp - s2 * ypq;
-                if (hq2) nxt[p1 * n + q2] = s2 * ypp + c2 * ypq;
-                if (hq1) nxt[q1 * n + p2] = c2 * yqp - s2 * yqq;
-                if (hq1 && hq2) nxt[q1 * n + q2] = s2 * yqp + c2 * yqq;
+                A[p1 * n + p2] = c2 * ypp - s2 * ypq;
+                if (hq2) A[p1 * n + q2] = s2 * ypp + c2 * ypq;
+                if (hq1) A[q1 * n + p2] = c2 * yqp - s2 * yqq;
+                if (hq1 && hq2) A[q1 * n + q2] = s2 * yqp + c2 * yqq;
             } else {
                 const double sv = sn[v];
                 if (sv == 0.0) continue;
@@ -275,10 +241,9 @@ __device__ double *cta_jacobi(double *A0, double *A1, double *V, int n, const Ar
             }
         }
         __syncthreads();
-        double *t = cur; cur = nxt; nxt = t;
     }
     *nsweeps = sweeps;
-    return cur;
+    return A;
 }
 
 // ascending order of diag(A) -> ar.perm (rank of each original index), stable by index
@@ -316,7 +281,7 @@ __global__ void __launch_bounds__(SCF_THREADS, 2) k_orth(DevBatch b, int nm) {
     __syncthreads();
     const long long t0 = clock64();
     int nsw = 0;
-    const double *Ad = cta_jacobi(ar.A, ar.W, ar.B, N, ar, &nsw);
+    const double *Ad = cta_jacobi(ar.A, ar.B, N, ar, &nsw);
     if (b.dbg && tid == 0) { b.dbg[16 * m + 12] = clock64() - t0; b.dbg[16 * m + 13] = nsw; }
     sort_eigs(Ad, N, ar);
     // kept = s > 1e-7, in ascending order: sorted positions [N - M, N)
@@ -346,6 +311,24 @@ __global__ void __launch_bounds__(SCF_THREADS, 2) k_orth(DevBatch b, int nm) {
 }
 
 
+// sum_{u < n} load(u) accumulated left to right (bitwise the plain loop's result), with
+// the loads issued 8 at a time: the partial reductions below read L2/HBM, and a serial
+// load-add chain left them latency-bound (~20% of the post kernel).
+template <typename F>
+__device__ __forceinline__ double seq_sum(int n, F load) {
+    double v = 0.0;
+    int u = 0;
+    for (; u + 8 <= n; u += 8) {
+        double x[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = load(u + k);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v += x[k];
+    }
+    for (; u < n; ++u) v += load(u);
+    return v;
+}
+
 // J from owner + scattered partials, K = -(G + G^T)/4 from G rows (fixed-order sums).
 __device__ void reduce_jk(const DevBatch &b, int m, int N, double *J, double *K) {
     const int tid = threadIdx.x;
@@ -353,8 +336,7 @@ __device__ void reduce_jk(const DevBatch &b, int m, int N, double *J, double *K)
     const double *Jp = b.Jpart + b.m_Jp0[m];
     const int ncj = b.m_jkcta0[m + 1] - b.m_jkcta0[m];
     for (int64_t q = tid; q < npp; q += SCF_THREADS) {
-        double v = 0.0;
-        for (int c = 0; c <= ncj; ++c) v += Jp[(int64_t)c * npp + q];
+        const double v = seq_sum(ncj + 1, [&](int c) { return Jp[(int64_t)c * npp + q]; });
         int k = (int)((sqrt(8.0 * (double)q + 1.0) - 1.0) * 0.5);
         while (tri(k + 1) <= q) ++k;
         while (tri(k) > q) --k;
@@ -365,9 +347,8 @@ __device__ void reduce_jk(const DevBatch &b, int m, int N, double *J, double *K)
     const double *Gp = b.Gpart + b.m_G0[m];
     for (int t = tid; t < N * N; t += SCF_THREADS) {
         const int a = t / N, c = t % N;
-        double v = 0.0;
-        for (int i = max(a, c); i < N; ++i) v += Gp[(tri(i) + a) * N + c];
-        K[t] = v;
+        const int i0 = max(a, c);
+        K[t] = seq_sum(N - i0, [&](int u) { return Gp[(tri(i0 + u) + a) * N + c]; });
     }
     __syncthreads();
     for (int t = tid; t < N * N; t += SCF_THREADS) {
@@ -388,9 +369,7 @@ __device__ void reduce_vxc(const DevBatch &b, int m, int N, double *Vx) {
     const double *Vp = b.Vpart + b.m_V0[m];
     const int ncx = b.m_xccta0[m + 1] - b.m_xccta0[m];
     for (int t = tid; t < N * N; t += SCF_THREADS) {
-        double v = 0.0;
-        for (int c = 0; c < ncx; ++c) v += Vp[(int64_t)c * N * N + t];
-        Vx[t] = v;
+        Vx[t] = seq_sum(ncx, [&](int c) { return Vp[(int64_t)c * N * N + t]; });
     }
     __syncthreads();
     for (int t = tid; t < N * N; t += SCF_THREADS) {
@@ -460,7 +439,7 @@ __device__ void diis_extrapolate(const DevBatch &b, int m, int N, const double *
     }
     __syncthreads();
     int nsw1 = 0;
-    const double *Ad = cta_jacobi(ar.A, ar.W, ar.B, n1, ar, &nsw1);
+    const double *Ad = cta_jacobi(ar.A, ar.B, n1, ar, &nsw1);
     if (tid == 0) {
         double mx = 0.0, mn = 1e308;
         for (int i = 0; i < n1; ++i) {
@@ -500,9 +479,17 @@ __device__ void diis_extrapolate(const DevBatch &b, int m, int N, const double *
         const double *Fp = b.Fring + (int64_t)slot(nh - 2) * tot + o;
         for (int t = tid; t < N * N; t += SCF_THREADS) Fuse[t] = 0.5 * Fl[t] + 0.5 * Fp[t];
     } else {
+        int64_t off[DIIS_MAX];
+#pragma unroll
+        for (int a = 0; a < DIIS_MAX; ++a) off[a] = (int64_t)slot(a < nh ? a : 0) * tot + o;
         for (int t = tid; t < N * N; t += SCF_THREADS) {
+            double x[DIIS_MAX];
+#pragma unroll
+            for (int a = 0; a < DIIS_MAX; ++a) x[a] = a < nh ? b.Fring[off[a] + t] : 0.0;
             double v = 0.0;
-            for (int a = 0; a < nh; ++a) v += ar.cf[a] * b.Fring[(int64_t)slot(a) * tot + o + t];
+#pragma unroll
+            for (int a = 0; a < DIIS_MAX; ++a)
+                if (a < nh) v += ar.cf[a] * x[a];
             Fuse[t] = v;
         }
     }
@@ -614,7 +601,7 @@ __global__ void __launch_bounds__(SCF_THREADS, 2) k_post(DevBatch b, PostArgs pa
         // f32 build: eigenvectors to f32 resolution (the reference's f32 path diagonalizes in
         // single precision, scf.py:86-98); f64 build: to 1e-13 of the largest |eigenvalue|
         int nsw = 0;
-        Ad = cta_jacobi(ar.A, ar.W, ar.B, M, ar, &nsw, 30, b.prec ? 1e-8 : 1e-13);
+        Ad = cta_jacobi(ar.A, ar.B, M, ar, &nsw, 30, b.prec ? 1e-8 : 1e-13);
         if (dbg && tid == 0) dbg[10] += nsw;
     }
     tick(4);
@@ -691,7 +678,7 @@ __global__ void __launch_bounds__(SCF_THREADS) k_roothaan(DevBatch b, int nm) {
     for (int t = tid; t < M * M; t += SCF_THREADS) ar.B[t] = (t / M == t % M) ? 1.0 : 0.0;
     __syncthreads();
     int nsw = 0;
-    const double *Ad = cta_jacobi(ar.A, ar.W, ar.B, M, ar, &nsw);
+    const double *Ad = cta_jacobi(ar.A, ar.B, M, ar, &nsw);
     sort_eigs(Ad, M, ar);
     for (int t = tid; t < M * M; t += SCF_THREADS) Cp[(t / M) * M + ar.perm[t % M]] = ar.B[t];
     for (int i = tid; i < M; i += SCF_THREADS) b.eps[(int64_t)m * NMAX + ar.perm[i]] = ar.dv[i];
@@ -737,7 +724,7 @@ __global__ void __launch_bounds__(SCF_THREADS) k_diis_single(const double *F, co
     }
     __syncthreads();
     int nsw2 = 0;
-    const double *Ad = cta_jacobi(ar.A, ar.W, ar.B, n1, ar, &nsw2);
+    const double *Ad = cta_jacobi(ar.A, ar.B, n1, ar, &nsw2);
     if (tid == 0) {
         double mx = 0.0, mn = 1e308;
         for (int i = 0; i < n1; ++i) { const double e = fabs(Ad[i * n1 + i]); mx = fmax(mx, e); mn = fmin(mn, e); }

@@ -2,7 +2,8 @@ import os, sys, numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2311_01135_b200 import synth, SCFOptions, load_basis
 from paper_2311_01135_b200.engine import Plan
-mols = synth.batch(8, 9, seed=1)
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+mols = synth.batch(n, 9, seed=1)
 for prec in ("f32", "f64"):
     opts = SCFOptions(max_iterations=20, convergence_std=0.0, grid_level=0, precision=prec)
     with Plan(mols, load_basis("sto-3g"), opts.engine()) as p:
