@@ -24,10 +24,20 @@
 // the f32 build (the reference's f32 BLAS path); the functional is always f64.
 #include "common.cuh"
 #include "b3lyp.cuh"
+#include "umma.cuh"
+#ifdef XC_PHASES
+#include <cstdio>
+#endif
 
 namespace dftb {
 
 constexpr int XC_THREADS = 256;
+// XC_MMA=1: f32 build runs the N 49..64 bucket on the tcgen05 kernel k_xc_mma below (parity
+// tests green on B200; measured 2.49 ms vs 2.27 ms per iteration for the FFMA kernel, so the
+// FFMA kernel stays the default - see DESIGN.md section 6, "measured and rejected")
+#ifndef XC_MMA
+#define XC_MMA 0
+#endif
 constexpr int XC_SHD = 13;       // doubles per shell record in smem
 
 template <typename W>
@@ -347,6 +357,399 @@ __global__ void __launch_bounds__(XC_THREADS) k_xc(DevBatch b, const int *ctas) 
     if (bad) atomicOr(b.status + m, DFTB_ST_XC_NONFINITE);
 }
 
+// ---------------------------------------------------------------------------- tensor cores
+// f32 build: the two N^2-per-point contractions on the 5th-generation tensor cores
+// (tcgen05.mma kind::tf32, accumulators in TMEM), everything else as in k_xc.
+//   t[p][nu]  = sum_mu phi[mu][p] rho[mu][nu]   M = 64 points, N = NP, K = NP AOs
+//   V[mu][nu] += sum_p phi[mu][p] wv[nu][p]     M = 64 / 128 AOs, N = NP, K = BP points
+// Precision: 3xTF32 (x = hi + lo, hi TF32 by round-to-nearest, lo the exact f32 remainder;
+// hi*lo + lo*hi + hi*hi per product, f32 accumulation): measured 5e-7 of the largest
+// element on random 64^3 products (tools/probe/umma_probe.cu); the reference's f32 path
+// is f32 BLAS.  Operands are K-major SWIZZLE_128B tiles (umma.cuh), so phi is kept in two
+// layouts: [mu][p] (V-phase A, and the FFMA consumers) and [p][mu] (t-phase A).
+// The CTA runs NG independent pipelines ("groups" of 256 threads, own tiles, own TMEM
+// accumulators and mbarriers, named barriers) over interleaved BP-point sub-blocks and
+// shares the density tiles: while one group waits on its MMAs or runs its (latency-bound,
+// f64) functional, the other computes AO values - the latency hiding of two CTAs per SM
+// without the second copy of rho.  One elected thread per group issues the MMAs.
+constexpr int XCG = 256;   // threads per group
+
+template <int NQ, int BP, int NG>
+struct XCM {
+    static constexpr int NP = 4 * NQ;
+    static constexpr int NSR = (NP + 31) / 32;     // 32-column segments of an AO-indexed row
+    static constexpr int NSP = BP / 32;            // 32-column segments of a point-indexed row
+    static constexpr int MV = NP <= 64 ? 64 : 128; // V-phase M
+    static constexpr int RHO = (NP / 8) * NSR * 256;       // floats per tile buffer
+    static constexpr int PHA = (BP / 8) * NSR * 256;       // [BP p rows][NP]  (M = 64 over-reads)
+    static constexpr int PHV = (NP / 8) * NSP * 256;       // [NP rows][BP]
+    static constexpr int GF = 2 * PHA + 7 * PHV;           // pha h/l, phv l/h, 3 dphi, wv h/l
+    static constexpr int EQ = BP / 16;                     // lane quarters holding points
+    static constexpr int NCS = NP / 2;                     // epilogue columns per warp
+    static_assert(BP == 32 || BP == 64, "sub-block size");
+    static_assert(4 * NP <= 256, "three t accumulators + V per group in 256 TMEM columns");
+    static_assert((64 - BP) / 8 * NSR * 256 <= 7 * PHV, "t-phase over-read stays in the group's tiles");
+    static_assert(MV == 64 || (128 - NP) / 8 * NSP * 256 <= 3 * PHV, "V-phase over-read stays in bounds");
+    static constexpr size_t grp(int g) { return 2 * (size_t)RHO + (size_t)g * GF; }
+    static constexpr size_t fend = 2 * (size_t)RHO + (size_t)NG * GF;
+    // per-group scalars (bytes): pt [BP][4] f64, dn [BP][4] f64, fpt [10][BP] f64 (the
+    // epilogue's [2][BP][4] f32 partials alias it), dw [4][BP] f32
+    static constexpr size_t GS = 160 * BP;
+    static constexpr size_t sc(int g) { return fend * 4 + (size_t)g * GS; }
+    static constexpr size_t red = fend * 4 + NG * GS;      // [32] f64
+    static constexpr size_t bars = red + 256;              // 2 NG mbarriers + TMEM base
+    static constexpr size_t shd = bars + 64;
+    // shell records: centres (f64, for the point - centre difference) and f32 exponents /
+    // coefficients (no per-use conversions in the AO loop)
+    static size_t bytes(int nsh) { return 1024 + shd + (8 * 3 + 4 * 10) * (size_t)nsh; }
+};
+
+__device__ __forceinline__ void gbar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+template <int NQ, int BP, int NG>
+__global__ void __launch_bounds__(NG * XCG, 1) k_xc_mma(DevBatch b, const int *ctas) {
+    using L = XCM<NQ, BP, NG>;
+    constexpr int NP = L::NP, NSR = L::NSR, NSP = L::NSP, MV = L::MV, NCS = L::NCS;
+    constexpr int NT = NG * XCG;
+    extern __shared__ __align__(16) unsigned char xsm_raw[];
+    // 1 KB-aligned base by pointer arithmetic on the shared array (an integer round trip would
+    // turn every access into a generic load / store)
+    unsigned char *xsm = xsm_raw + ((1024u - (umma::saddr(xsm_raw) & 1023u)) & 1023u);
+    float *fs = (float *)xsm;
+    float *rho_h = fs, *rho_l = fs + L::RHO;
+    double *red = (double *)(xsm + L::red), *shd = (double *)(xsm + L::shd);
+    uint64_t *bars = (uint64_t *)(xsm + L::bars);
+    uint32_t *tbase = (uint32_t *)(bars + 2 * NG);
+    const int cta = ctas[blockIdx.x];
+    const int m = b.xc_mol[cta];
+    if (b.done[m]) return;
+    const int N = b.m_nao[m];
+    const int nsh = b.m_nshell[m], s0 = b.m_shell0[m];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // ---- setup: rho (K-major rows nu, cols mu) split, zeroed tiles, shell records
+    const double *rg = b.rho + b.m_mat0[m];
+    for (int t = tid; t < NP * NP; t += NT) {
+        const int nu = t / NP, mu = t % NP;
+        const float x = (nu < N && mu < N) ? (float)rg[mu * N + nu] : 0.f;
+        const float h = umma::tf32_hi(x);
+        const int o = umma::sw128(nu, mu, NSR);
+        rho_h[o] = h;
+        rho_l[o] = x - h;
+    }
+    for (int t = tid; t < NG * L::GF; t += NT) fs[L::grp(0) + t] = 0.f;
+    float *shf = (float *)(shd + 3 * nsh);   // [nsh][10]: exps, cs, cp, (ao << 1 | kind) bits
+    for (int sh = tid; sh < nsh; sh += NT) {
+        const int gsh = s0 + sh;
+        double *r = shd + 3 * sh;
+        float *f = shf + 10 * sh;
+        const double *A = b.a_xyz + 3 * b.s_atom[gsh];
+        for (int d = 0; d < 3; ++d) {
+            r[d] = A[d];
+            f[d] = (float)b.s_exp[3 * gsh + d];
+            f[3 + d] = (float)b.s_cs[3 * gsh + d];
+            f[6 + d] = (float)b.s_cp[3 * gsh + d];
+        }
+        f[9] = __int_as_float((b.s_ao[gsh] << 1) | (b.s_kind[gsh] & 1));
+    }
+    if (warp == 0) umma::tmem_alloc(tbase, NG == 1 ? 256 : 512);
+    if (tid == 0) {
+        for (int k = 0; k < 2 * NG; ++k) umma::mbar_init(bars + k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    umma::fence_async_smem();
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    // ---- this thread's group
+    const int g = tid / XCG, tl = tid % XCG, wl = tl >> 5;
+    const int gid = 1 + g, gfun = 1 + NG + g;                 // named barriers
+    float *G = fs + L::grp(g);
+    float *pha_h = G, *pha_l = G + L::PHA, *phv_l = G + 2 * L::PHA, *phv_h = phv_l + L::PHV;
+    float *dphi = phv_h + L::PHV, *wv_h = dphi + 3 * L::PHV, *wv_l = wv_h + L::PHV;
+    double *pt = (double *)(xsm + L::sc(g)), *dn = pt + 4 * BP, *fpt = dn + 4 * BP;
+    float *part = (float *)fpt, *dw = (float *)(fpt + 10 * BP);
+    uint64_t *bar_t = bars + 2 * g, *bar_v = bar_t + 1;
+    // TMEM per group: three t accumulators (hi*lo, lo*hi, hi*hi: three independent MMA chains
+    // instead of one dependent chain of 3 NP/8 MMAs), then V
+    const uint32_t TT = *tbase + 256 * g, TV = TT + 3 * NP;
+    const uint32_t sbr = NSR * 1024, sbp = NSP * 1024;
+    const uint64_t dpha_h = umma::desc_sw128(umma::saddr(pha_h), sbr), dpha_l = umma::desc_sw128(umma::saddr(pha_l), sbr);
+    const uint64_t drho_h = umma::desc_sw128(umma::saddr(rho_h), sbr), drho_l = umma::desc_sw128(umma::saddr(rho_l), sbr);
+    const uint64_t dphv_h = umma::desc_sw128(umma::saddr(phv_h), sbp), dphv_l = umma::desc_sw128(umma::saddr(phv_l), sbp);
+    const uint64_t dwv_h = umma::desc_sw128(umma::saddr(wv_h), sbp), dwv_l = umma::desc_sw128(umma::saddr(wv_l), sbp);
+    constexpr uint32_t IT = umma::idesc_tf32(64, NP), IV = umma::idesc_tf32(MV, NP);
+    double e_acc = 0.0;
+    int bad = 0;
+    const int64_t p0 = b.xc_p0[cta], p1 = b.xc_p1[cta];
+    int s = 0;
+#ifdef XC_PHASES
+    long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tck = clock64();
+#define XPH(k) do { const long long t_ = clock64(); ph[k] += t_ - tck; tck = t_; } while (0)
+#else
+#define XPH(k) do { } while (0)
+#endif
+    for (int64_t sb = p0 + (int64_t)g * BP; sb < p1; sb += (int64_t)NG * BP, ++s) {
+        const int nb = (int)min((int64_t)BP, p1 - sb);
+        if (s > 0 && wl == 0) umma::mbar_wait(bar_v, (uint32_t)((s - 1) & 1));   // V MMAs done with phi, wv
+        if (tl < BP) {
+            const int64_t gi = sb + min(tl, nb - 1);
+            pt[4 * tl] = b.g_xyz[3 * gi];
+            pt[4 * tl + 1] = b.g_xyz[3 * gi + 1];
+            pt[4 * tl + 2] = b.g_xyz[3 * gi + 2];
+            pt[4 * tl + 3] = tl < nb ? b.g_w[gi] : 0.0;
+        }
+        gbar(gid, XCG);
+        XPH(0);
+        // ---- AO values and gradients (f32) -> both phi layouts (hi / lo) + gradient planes
+        for (int t = tl; t < BP * nsh; t += XCG) {
+            const int p = t % BP, sh = t / BP;
+            const double *r = shd + 3 * sh;
+            const float *f = shf + 10 * sh;
+            const int kao = __float_as_int(f[9]), kind = kao & 1, ao = kao >> 1;
+            float v[4][4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) v[a][c] = 0.f;
+            if (p < nb) {
+                const double *q = pt + 4 * p;
+                const float dx = (float)(q[0] - r[0]), dy = (float)(q[1] - r[1]), dz = (float)(q[2] - r[2]);
+                const float r2 = dx * dx + dy * dy + dz * dz;
+                float bs = 0, ds = 0, bp = 0, dp = 0;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const float a = f[k];
+                    const float ar = a * r2;
+                    const float e = ar < 88.f ? expf(-ar) : 0.f;
+                    const float m2a = -2.f * a;
+                    bs += f[3 + k] * e;
+                    ds += f[3 + k] * m2a * e;
+                    bp += f[6 + k] * e;
+                    dp += f[6 + k] * m2a * e;
+                }
+                const float rel[3] = {dx, dy, dz};
+                v[0][0] = bs;
+#pragma unroll
+                for (int d = 0; d < 3; ++d) v[d + 1][0] = rel[d] * ds;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    v[0][1 + c] = rel[c] * bp;
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) v[d + 1][1 + c] = (c == d ? bp : 0.f) + rel[c] * rel[d] * dp;
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                if (c > 0 && !kind) break;
+                const float x = v[0][c], h = umma::tf32_hi(x);
+                const int ov = umma::sw128(ao + c, p, NSP), oa = umma::sw128(p, ao + c, NSR);
+                phv_h[ov] = h;
+                phv_l[ov] = x - h;
+                pha_h[oa] = h;
+                pha_l[oa] = x - h;
+#pragma unroll
+                for (int d = 0; d < 3; ++d) dphi[d * L::PHV + ov] = v[d + 1][c];
+            }
+        }
+        umma::fence_async_smem();
+        umma::fence_before();
+        gbar(gid, XCG);
+        XPH(1);
+        if (tl == 0) {   // ---- t = phi^T rho on the tensor cores
+            umma::fence_after();
+#pragma unroll
+            for (int k = 0; k < NP / 8; ++k) {
+                const uint64_t ah = umma::desc_step(dpha_h, k), al = umma::desc_step(dpha_l, k);
+                const uint64_t bh = umma::desc_step(drho_h, k), bl = umma::desc_step(drho_l, k);
+                umma::mma_tf32(TT, ah, bl, IT, k > 0);
+                umma::mma_tf32(TT + NP, al, bh, IT, k > 0);
+                umma::mma_tf32(TT + 2 * NP, ah, bh, IT, k > 0);
+            }
+            umma::commit(bar_t);
+        }
+        if (wl == 0) umma::mbar_wait(bar_t, (uint32_t)(s & 1));
+        gbar(gid, XCG);
+        umma::fence_after();
+        XPH(2);
+        {   // ---- n, grad n partials: warp -> lane quarter q (points 16q..16q+15), column half c
+            const int q = warp & 3, c = wl >> 2;
+            if (q < L::EQ) {
+                float tv[NCS];
+#pragma unroll
+                for (int j = 0; j < NCS / 16; ++j) {
+                    float a16[16], b16[16], c16[16];
+                    const uint32_t ta = TT + ((uint32_t)(32 * q) << 16) + (uint32_t)(c * NCS + 16 * j);
+                    umma::tld16(ta, a16);
+                    umma::tld16(ta + NP, b16);
+                    umma::tld16(ta + 2 * NP, c16);
+                    umma::tld_wait();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) tv[16 * j + i] = (a16[i] + b16[i]) + c16[i];
+                }
+                const int p = 16 * q + lane;
+                if (lane < 16) {
+                    float n = 0.f, gx = 0.f, gy = 0.f, gz = 0.f;
+#pragma unroll
+                    for (int i = 0; i < NCS; ++i) {
+                        const int o = umma::sw128(c * NCS + i, p, NSP);
+                        const float f = phv_h[o] + phv_l[o];
+                        n += tv[i] * f;
+                        gx += tv[i] * dphi[o];
+                        gy += tv[i] * dphi[L::PHV + o];
+                        gz += tv[i] * dphi[2 * L::PHV + o];
+                    }
+                    float *pp = part + 4 * (c * BP + p);
+                    pp[0] = n; pp[1] = gx; pp[2] = gy; pp[3] = gz;
+                }
+            }
+        }
+        umma::fence_before();
+        gbar(gid, XCG);
+        if (tl < BP) {   // fixed-order combine of the two column halves
+            const float *pa = part + 4 * tl, *pb = part + 4 * (BP + tl);
+            double *d = dn + 4 * tl;
+            d[0] = (double)(pa[0] + pb[0]);
+            d[1] = (double)(2.f * (pa[1] + pb[1]));
+            d[2] = (double)(2.f * (pa[2] + pb[2]));
+            d[3] = (double)(2.f * (pa[3] + pb[3]));
+        }
+        gbar(gid, XCG);
+        XPH(3);
+        if (tl < 3 * BP) {   // ---- functional (f64): three parts on three thread groups
+            const int pt_i = tl % BP, prt = tl / BP;
+            const double *dq = dn + 4 * pt_i;
+            double n = dq[0], sig = 0.0;
+            {
+                const float gx = (float)dq[1], gy = (float)dq[2], gz = (float)dq[3];
+                sig = (double)(gx * gx + gy * gy + gz * gz);
+            }
+            const bool ok = pt_i < nb && b3lyp_clamp(n, sig);
+            if (prt == 1) {
+                const VPart v = ok ? b3lyp_vwn(n) : VPart{0.0, 0.0};
+                fpt[5 * BP + pt_i] = v.f2;
+                fpt[6 * BP + pt_i] = v.v2;
+            } else if (prt == 2) {
+                const LPart l = ok ? b3lyp_lyp(n, sig) : LPart{0.0, 0.0, 0.0};
+                fpt[7 * BP + pt_i] = l.f3;
+                fpt[8 * BP + pt_i] = l.v3;
+                fpt[9 * BP + pt_i] = l.w3;
+            }
+            XPart x{0.0, 0.0, 0.0, 0.0, 0.0};
+            if (prt == 0 && ok) x = b3lyp_x(n, sig);
+            gbar(gfun, 3 * BP);
+            if (prt == 0) {
+                if (ok) {
+                    const double gx = dq[1], gy = dq[2], gz = dq[3];
+                    const XCOut o = xc_combine(n, x, VPart{fpt[5 * BP + pt_i], fpt[6 * BP + pt_i]},
+                                               LPart{fpt[7 * BP + pt_i], fpt[8 * BP + pt_i], fpt[9 * BP + pt_i]});
+                    if (!(isfinite(o.exc) && isfinite(o.vrho) && isfinite(o.vsigma))) bad = 1;
+                    const double w = pt[4 * pt_i + 3];
+                    e_acc += w * n * (double)(float)o.exc;
+                    const double ww = (double)(float)w;
+                    const double a = (double)(float)(0.5 * ww * (double)(float)o.vrho);
+                    const double bb = (double)(float)(2.0 * ww * (double)(float)o.vsigma);
+                    dw[pt_i] = (float)a;
+                    dw[BP + pt_i] = (float)(bb * gx);
+                    dw[2 * BP + pt_i] = (float)(bb * gy);
+                    dw[3 * BP + pt_i] = (float)(bb * gz);
+                } else {
+                    dw[pt_i] = dw[BP + pt_i] = dw[2 * BP + pt_i] = dw[3 * BP + pt_i] = 0.f;
+                }
+            }
+        }
+        gbar(gid, XCG);
+        XPH(4);
+        {   // ---- wv = a phi + b . grad phi (split); this thread's point is fixed
+            const int p = tl % BP;
+            const float d0 = dw[p], d1 = dw[BP + p], d2 = dw[2 * BP + p], d3 = dw[3 * BP + p];
+            for (int nu = tl / BP; nu < NP; nu += XCG / BP) {
+                const int o = umma::sw128(nu, p, NSP);
+                const float w = d0 * (phv_h[o] + phv_l[o]) + d1 * dphi[o] + d2 * dphi[L::PHV + o] +
+                                d3 * dphi[2 * L::PHV + o];
+                const float h = umma::tf32_hi(w);
+                wv_h[o] = h;
+                wv_l[o] = w - h;
+            }
+        }
+        umma::fence_async_smem();
+        umma::fence_before();
+        gbar(gid, XCG);
+        if (tl == 0) {   // ---- V += phi wv^T on the tensor cores (accumulated in TMEM)
+            umma::fence_after();
+#pragma unroll
+            for (int k = 0; k < BP / 8; ++k) {
+                const uint64_t ah = umma::desc_step(dphv_h, k), al = umma::desc_step(dphv_l, k);
+                const uint64_t bh = umma::desc_step(dwv_h, k), bl = umma::desc_step(dwv_l, k);
+                umma::mma_tf32(TV, ah, bl, IV, (s > 0 || k > 0) ? 1u : 0u);
+                umma::mma_tf32(TV, al, bh, IV, 1);
+                umma::mma_tf32(TV, ah, bh, IV, 1);
+            }
+            umma::commit(bar_v);
+        }
+        XPH(5);
+    }
+#ifdef XC_PHASES
+    if (blockIdx.x < 2 && tl == 0)
+        printf("xc cta %d group %d subblocks %d: pts+wait %lld  phi %lld  tmma %lld  epi %lld  func %lld  wv+vmma %lld\n",
+               blockIdx.x, g, s, ph[0], ph[1], ph[2], ph[3], ph[4], ph[5]);
+#endif
+    if (s > 0 && wl == 0) umma::mbar_wait(bar_v, (uint32_t)((s - 1) & 1));
+    __syncthreads();
+    umma::fence_after();
+    // ---- V partial = sum of the groups' accumulators (fixed order) -> f64 global
+    const int nsb = (int)((p1 - p0 + BP - 1) / BP);        // sub-blocks of the CTA; group k ran ceil((nsb - k) / NG)
+    const int local = cta - b.m_xccta0[m];
+    double *Vp = b.Vpart + b.m_V0[m] + (int64_t)local * N * N;
+    {
+        constexpr int NW = NT / 32, NSPL = NW / 4, CPW = NP / NSPL;   // column split over the warps
+        const int q = warp & 3, c = warp >> 2;
+        float acc[CPW];
+#pragma unroll
+        for (int i = 0; i < CPW; ++i) acc[i] = 0.f;
+        for (int k = 0; k < NG; ++k) {
+            if (k >= nsb) break;
+            const uint32_t base = *tbase + 256 * k + 3 * NP + ((uint32_t)(32 * q) << 16) + (uint32_t)(c * CPW);
+#pragma unroll
+            for (int j = 0; j < CPW / 16; ++j) {
+                float t16[16];
+                umma::tld16(base + 16 * j, t16);
+                umma::tld_wait();
+#pragma unroll
+                for (int i = 0; i < 16; ++i) acc[16 * j + i] += t16[i];
+            }
+            if constexpr (CPW % 16) {
+                float t4[4];
+                umma::tld4(base + (CPW / 16) * 16, t4);
+                umma::tld_wait();
+#pragma unroll
+                for (int i = 0; i < 4; ++i) acc[(CPW / 16) * 16 + i] += t4[i];
+            }
+        }
+        const int mu = MV == 64 ? (lane < 16 ? 16 * q + lane : NP) : 32 * q + lane;
+        if (mu < N)
+#pragma unroll
+            for (int i = 0; i < CPW; ++i) {
+                const int nu = c * CPW + i;
+                if (nu < N) Vp[mu * N + nu] = (double)acc[i];
+            }
+    }
+    umma::fence_before();
+    const double e = block_sum(e_acc, red);
+    if (tid == 0) b.Epart[cta] = e;
+    if (bad) atomicOr(b.status + m, DFTB_ST_XC_NONFINITE);
+    if (warp == 0) {
+        umma::fence_after();
+        umma::tmem_free(*tbase, NG == 1 ? 256 : 512);
+    }
+}
+
+template <int NQ, int BP, int NG>
+static void launch_bucket_mma(const DevBatch &b, const int *ctas, int n, int nsh_max, cudaStream_t s) {
+    const size_t sm = XCM<NQ, BP, NG>::bytes(nsh_max);
+    cudaFuncSetAttribute(k_xc_mma<NQ, BP, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_xc_mma<NQ, BP, NG><<<n, NG * XCG, sm, s>>>(b, ctas);
+}
+
 template <typename W, int NQ, int BP>
 static void launch_bucket(const DevBatch &b, const int *ctas, int n, int nsh_max, cudaStream_t s) {
     const size_t sm = XCL<W, NQ, BP>::bytes(nsh_max);
@@ -366,9 +769,18 @@ static void launch_xc_t(const DevBatch &b, const int *bucket_ctas, const int *bu
     c += bucket_n[1];
     if (bucket_n[2]) launch_bucket<W, 12, BP>(b, c, bucket_n[2], nsh_max, s);
     c += bucket_n[2];
-    if (bucket_n[3]) launch_bucket<W, 16, BP>(b, c, bucket_n[3], nsh_max, s);
-    c += bucket_n[3];
-    if (bucket_n[4]) launch_bucket<W, 20, BPL>(b, c, bucket_n[4], nsh_max, s);
+#if XC_MMA
+    if constexpr (sizeof(W) == 4) {
+        if (bucket_n[3]) launch_bucket_mma<16, 32, 2>(b, c, bucket_n[3], nsh_max, s);
+        c += bucket_n[3];
+        if (bucket_n[4]) launch_bucket<W, 20, BPL>(b, c, bucket_n[4], nsh_max, s);
+    } else
+#endif
+    {
+        if (bucket_n[3]) launch_bucket<W, 16, BP>(b, c, bucket_n[3], nsh_max, s);
+        c += bucket_n[3];
+        if (bucket_n[4]) launch_bucket<W, 20, BPL>(b, c, bucket_n[4], nsh_max, s);
+    }
     c += bucket_n[4];
     if (bucket_n[5]) launch_bucket<W, 24, BPL>(b, c, bucket_n[5], nsh_max, s);
 }
