@@ -160,7 +160,8 @@ int dftb_fma_peak(int fp64, double *tflops, void *stream);
 /* Kernel-level timing for roofline reporting: re-runs the J/K digestion and the XC
  * kernels (pure functions of the device-resident density; they only rewrite their own
  * partials) `reps` times between CUDA events on `stream` and returns the average time of
- * one J/K launch set and of one XC launch set (ms).  Requires a completed dftb_plan_run. */
+ * one J/K launch set and of one XC launch set (ms).  Requires a completed dftb_plan_run, or
+ * (ms_xc == NULL: J/K only) a dense store from dftb_plan_eri and a density from dftb_plan_jk. */
 int dftb_plan_kernel_times(dftb_plan *plan, int32_t reps, double *ms_jk, double *ms_xc, void *stream);
 
 #ifdef __cplusplus

@@ -36,11 +36,14 @@ HD constexpr int hidx(int t, int u, int v) {
 }
 
 // F_0..F_L(T); tab = 431 x 16 table of F_m at T = 0.1 k (boys.cu).  Mirrors _kernels.py:48-68.
+// exp(-T) is evaluated once, before the branch: quartets of one warp mix small and large T,
+// and with an exp in each branch a divergent warp paid for two (for T >= 700 exp(-T) is
+// below 1e-304 and leaves the asymptotic recursion unchanged, as the former explicit zero did)
 template <int L>
 HD void boys(double T, double *F, const double *tab) {
+    const double et = exp(-T);
     if (T > 42.95) {
         double f = 0.5 * sqrt(kPi / T);
-        double et = T < 700.0 ? exp(-T) : 0.0;
         double h = 0.5 / T;
         F[0] = f;
 #pragma unroll
@@ -53,7 +56,6 @@ HD void boys(double T, double *F, const double *tab) {
 #pragma unroll
         for (int j = 6; j > 0; --j) acc = (acc + row[j]) * (-dT) * (1.0 / j);
         F[L] = acc + row[0];
-        double et = exp(-T);
 #pragma unroll
         for (int m = L - 1; m >= 0; --m) F[m] = (2.0 * T * F[m + 1] + et) * (1.0 / (2 * m + 1));
     }

@@ -949,7 +949,7 @@ int dftb_diis(const double *F, const double *E, int32_t m, int32_t n, double *ou
 }
 
 int dftb_plan_kernel_times(dftb_plan *p, int32_t reps, double *ms_jk, double *ms_xc, void *stream) {
-    if (!p || reps < 1 || !ms_jk || !ms_xc) return fail(DFTB_EINVAL, "bad arguments");
+    if (!p || reps < 1 || !ms_jk) return fail(DFTB_EINVAL, "bad arguments");
     cudaStream_t st = (cudaStream_t)stream;
     const DevBatch &d = p->d;
     // the kernels skip molecules whose SCF has finished: clear the flags for the timing
@@ -960,19 +960,21 @@ int dftb_plan_kernel_times(dftb_plan *p, int32_t reps, double *ms_jk, double *ms
     CK(cudaMemsetAsync(d.done, 0, sizeof(int) * d.n_mol, st));
     cudaEvent_t e[3];
     for (auto &x : e) CK(cudaEventCreate(&x));
+    const bool xc = ms_xc != nullptr;     // null: J/K only (no grid needed)
     launch_jk(d, p->jk_bucket_ctas, p->jk_bucket_n, st);                 // warm
-    launch_xc(d, p->xc_bucket_ctas, p->xc_bucket_n, p->nsh_max, st);
+    if (xc) launch_xc(d, p->xc_bucket_ctas, p->xc_bucket_n, p->nsh_max, st);
     CK(cudaEventRecord(e[0], st));
     for (int r = 0; r < reps; ++r) launch_jk(d, p->jk_bucket_ctas, p->jk_bucket_n, st);
     CK(cudaEventRecord(e[1], st));
-    for (int r = 0; r < reps; ++r) launch_xc(d, p->xc_bucket_ctas, p->xc_bucket_n, p->nsh_max, st);
+    if (xc)
+        for (int r = 0; r < reps; ++r) launch_xc(d, p->xc_bucket_ctas, p->xc_bucket_n, p->nsh_max, st);
     CK(cudaEventRecord(e[2], st));
     CK(cudaEventSynchronize(e[2]));
     float a = 0.f, c = 0.f;
     CK(cudaEventElapsedTime(&a, e[0], e[1]));
     CK(cudaEventElapsedTime(&c, e[1], e[2]));
     *ms_jk = a / reps;
-    *ms_xc = c / reps;
+    if (xc) *ms_xc = c / reps;
     for (auto &x : e) cudaEventDestroy(x);
     CK(cudaMemcpyAsync(d.done, done.data(), sizeof(int) * d.n_mol, cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));

@@ -116,12 +116,26 @@ class Plan:
     def iterate(self, it: int):
         _lib.check(self.lib.dftb_plan_iterate(self.h, int(it), self.stream))
 
-    def kernel_times(self, reps: int = 5) -> tuple[float, float]:
-        """(ms per J/K launch set, ms per XC launch set) re-run on the resident density."""
-        jk, xc = ctypes.c_double(0.0), ctypes.c_double(0.0)
-        _lib.check(self.lib.dftb_plan_kernel_times(self.h, int(reps), ctypes.byref(jk), ctypes.byref(xc),
-                                                   self.stream))
-        return jk.value, xc.value
+    def kernel_times(self, reps: int = 5, xc: bool = True) -> tuple[float, float | None]:
+        """(ms per J/K launch set, ms per XC launch set or None) re-run on the resident density."""
+        jk, x = ctypes.c_double(0.0), ctypes.c_double(0.0)
+        _lib.check(self.lib.dftb_plan_kernel_times(self.h, int(reps), ctypes.byref(jk),
+                                                   ctypes.byref(x) if xc else None, self.stream))
+        return jk.value, (x.value if xc else None)
+
+    def eri(self, screened: bool = True):
+        """Operator stage: pair tables, Schwarz bounds and the dense ERI store (dftb_plan_eri)."""
+        _lib.check(self.lib.dftb_plan_eri(self.h, 1 if screened else 0, self.stream))
+
+    def jk(self, rho: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+        """Operator stage: J, K of the whole batch for host densities (dftb_plan_jk)."""
+        n = int(np.sum(np.asarray(self.pk.mol_nao, dtype=np.int64) ** 2))
+        r = np.ascontiguousarray(rho, np.float64).reshape(-1)
+        if r.size != n:
+            raise DimensionError(f"rho has {r.size} elements, the batch needs {n}")
+        J, K = np.empty(n), np.empty(n)
+        _lib.check(self.lib.dftb_plan_jk(self.h, _lib.ptr(r), _lib.ptr(J), _lib.ptr(K), self.stream))
+        return J, K
 
     def set_timing(self, on: bool = True):
         _lib.check(self.lib.dftb_plan_set_timing(self.h, 1 if on else 0))
