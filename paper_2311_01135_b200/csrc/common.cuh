@@ -3,6 +3,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <type_traits>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "../../include/qm1b_b200.h"
 
@@ -48,6 +51,25 @@ HD int64_t eri_pos(int i, int j, int k, int l) {
     return eri_row(i, j) + eri_ket(k, l);
 }
 HD int64_t eri_size(int N) { return eri_slab0(N); }
+
+// Opt a kernel in to the device's full dynamic shared memory, once per (kernel, device).
+// The attribute is process-global state: setting it per launch to a batch-dependent size
+// raced between the pipeline's host threads (one plan per thread, batches with different
+// AO counts): a thread could launch after another had lowered the limit ("invalid argument" /
+// "too many resources requested for launch").  A launch still reserves only its own size.
+inline void smem_optin(const void *fn) {
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    if (!done.insert({fn, dev}).second) return;
+    cudaFuncAttributes a;
+    int optin = 0;
+    cudaFuncGetAttributes(&a, fn);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)a.sharedSizeBytes);
+}
 
 // Device-resident view of one batch.  Every pointer is a device pointer owned by
 // the plan (plan.cu).  Index conventions: "global" = over the whole batch,

@@ -293,7 +293,7 @@ static void launch_cls(const DevBatch &b, int cls, int64_t n, double eps, double
     constexpr int NKET = (KC ? 4 : 1) * (KD ? 4 : 1), NSL = NKET / (KPS ? KPS : NKET);
     const size_t sm = KSM ? sizeof(double) * KetSmem<(KC || KD), NS>::NSLOT * 9 * ERI_T : 0;
     auto kern = k_eri<KA, KB, KC, KD, KPS, ST, KSM, MINB, NS>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    smem_optin((const void *)kern);
     kern<<<dim3(nblk(n, ERI_T), NSL), ERI_T, sm, s>>>(b, cls, eps, prim_cut, eri);
     ++*nlaunch;
 }

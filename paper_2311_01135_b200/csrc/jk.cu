@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, const int *ctas) 
 template <typename ST, int NB>
 static void launch_bucket(const DevBatch &b, const int *ctas, int n, cudaStream_t s) {
     const size_t sm = JKPlan<ST, NB>::bytes;
-    cudaFuncSetAttribute(k_jk<ST, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    smem_optin((const void *)k_jk<ST, NB>);
     k_jk<ST, NB><<<n, JK_THREADS, sm, s>>>(b, ctas);
 }
 

@@ -651,7 +651,7 @@ static int arena_dim(int nmax) { return nmax < 16 ? 16 : nmax; }
 void launch_orth(const DevBatch &b, int nmax, cudaStream_t s) {
     const int nm = arena_dim(nmax);
     const size_t sm = scf_smem_bytes(nm);
-    cudaFuncSetAttribute(k_orth, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    smem_optin((const void *)k_orth);
     k_orth<<<b.n_mol, SCF_THREADS, sm, s>>>(b, nm);
 }
 
@@ -659,7 +659,7 @@ void launch_post(const DevBatch &b, int nmax, int it, int diis_start, int diis_h
                  double conv_std, cudaStream_t s) {
     const int nm = arena_dim(nmax);
     const size_t sm = scf_smem_bytes(nm);
-    cudaFuncSetAttribute(k_post, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    smem_optin((const void *)k_post);
     PostArgs pa{nm, it, diis_start, diis_hist, damping, conv_std};
     k_post<<<b.n_mol, SCF_THREADS, sm, s>>>(b, pa);
 }
@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(SCF_THREADS) k_roothaan(DevBatch b, int nm) {
 void launch_roothaan(const DevBatch &b, int nmax, cudaStream_t s) {
     const int nm = arena_dim(nmax);
     const size_t sm = scf_smem_bytes(nm);
-    cudaFuncSetAttribute(k_roothaan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    smem_optin((const void *)k_roothaan);
     k_roothaan<<<b.n_mol, SCF_THREADS, sm, s>>>(b, nm);
 }
 
@@ -763,7 +763,7 @@ __global__ void __launch_bounds__(SCF_THREADS) k_diis_single(const double *F, co
 
 void launch_diis_single(const double *F, const double *E, int mh, int n, double *out, cudaStream_t s) {
     const size_t sm = scf_smem_bytes(max(mh + 1, 16));
-    cudaFuncSetAttribute(k_diis_single, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    smem_optin((const void *)k_diis_single);
     k_diis_single<<<1, SCF_THREADS, sm, s>>>(F, E, mh, n, out);
 }
 

@@ -135,7 +135,7 @@ void launch_onee(const DevBatch &b, cudaStream_t s) {
 }
 void launch_grid(const DevBatch &b, int max_atoms, cudaStream_t s) {
     const size_t sm = sizeof(double) * ((size_t)max_atoms * max_atoms + 3 * max_atoms);
-    if (sm > 48 * 1024) cudaFuncSetAttribute(k_grid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    smem_optin((const void *)k_grid);
     if (b.n_atom) k_grid<<<b.n_atom, 256, sm, s>>>(b);
 }
 

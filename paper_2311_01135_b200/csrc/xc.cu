@@ -746,14 +746,14 @@ __global__ void __launch_bounds__(NG * XCG, 1) k_xc_mma(DevBatch b, const int *c
 template <int NQ, int BP, int NG>
 static void launch_bucket_mma(const DevBatch &b, const int *ctas, int n, int nsh_max, cudaStream_t s) {
     const size_t sm = XCM<NQ, BP, NG>::bytes(nsh_max);
-    cudaFuncSetAttribute(k_xc_mma<NQ, BP, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    smem_optin((const void *)k_xc_mma<NQ, BP, NG>);
     k_xc_mma<NQ, BP, NG><<<n, NG * XCG, sm, s>>>(b, ctas);
 }
 
 template <typename W, int NQ, int BP>
 static void launch_bucket(const DevBatch &b, const int *ctas, int n, int nsh_max, cudaStream_t s) {
     const size_t sm = XCL<W, NQ, BP>::bytes(nsh_max);
-    cudaFuncSetAttribute(k_xc<W, NQ, BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    smem_optin((const void *)k_xc<W, NQ, BP>);
     k_xc<W, NQ, BP><<<n, XC_THREADS, sm, s>>>(b, ctas);
 }
 

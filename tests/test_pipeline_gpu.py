@@ -60,3 +60,22 @@ def test_label_batches_in_flight(gpu_lib):
     for k in (0, 4):                                # same labels as a lone batch
         ref = [r.E_total for r in scf_batch(batches[k], b, opts)]
         assert [r.E_total for r in got[k]] == ref
+
+
+def test_mixed_size_batches_in_flight(gpu_lib):
+    """Batches with different AO counts / shell counts in flight at once (different shared-
+    memory sizes for the same kernels from several host threads): no batch may fail, and
+    every batch's labels equal those of the batch run alone."""
+    from paper_2311_01135_b200 import synth
+
+    b = load_basis("sto-3g")
+    opts = SCFOptions(max_iterations=6, convergence_std=0.0, grid_level=0, precision="f32")
+    heavy = [2, 11, 3, 10, 2, 11, 4, 9, 2, 11]
+    batches = [synth.batch(8, h, seed=40 + k) for k, h in enumerate(heavy)]
+    got = {k: res for k, res, _ in label_batches(batches, b, opts, workers=4)}
+    assert sorted(got) == list(range(len(batches)))
+    for k, res in got.items():
+        assert not any(isinstance(r, Exception) for r in res), (k, [r for r in res if isinstance(r, Exception)][:1])
+    for k in (1, 2):
+        ref = [r.E_total for r in scf_batch(batches[k], b, opts)]
+        assert [r.E_total for r in got[k]] == ref
