@@ -101,11 +101,11 @@ struct JKPlan {
     static constexpr size_t cap = 227 * 1024;
     // resident CTAs per SM by shared memory (1 KB per-CTA reservation)
     static constexpr int ctas(size_t bytes) { return (int)((228 * 1024) / (bytes + 1024)); }
-    // double-buffer unless a single stage buffer raises the CTAs per SM (NB <= 64: the
-    // bulk of the work; measured on B200 for NB = 64 f32: 2 -> 3 CTAs, J/K 1.66 -> 1.56 ms)
+    // double-buffer unless a single stage buffer raises the CTAs per SM (measured on B200:
+    // NB = 64 f32 2 -> 3 CTAs, J/K 1.66 -> 1.56 ms; NB = 80 f32 1 -> 2 CTAs)
     static constexpr int NBUF =
         JK_NBUF_MAX > 1 && fixed + 2 * JK_WARPS * row_bytes <= cap &&
-                !(NB <= 64 && ctas(fixed + JK_WARPS * row_bytes) > ctas(fixed + 2 * JK_WARPS * row_bytes))
+                !(ctas(fixed + JK_WARPS * row_bytes) > ctas(fixed + 2 * JK_WARPS * row_bytes))
             ? 2 : 1;
     static constexpr int CR = fixed + NBUF * JK_WARPS * row_bytes <= cap ? JK_WARPS : JK_WARPS / 2;
     static constexpr size_t bytes = fixed + NBUF * CR * row_bytes;
