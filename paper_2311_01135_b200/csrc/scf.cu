@@ -147,12 +147,16 @@ __device__ void cta_gemm(double *C, int ldc, const double *A, int lda, bool tA, 
 // Cyclic Jacobi, round-robin (circle) pairing: n/2 disjoint rotations per step,
 // applied at once as J^T A J on 2x2 blocks (rows of pair k1 x columns of pair k2), in
 // place: the blocks partition A, so every element is read and written by exactly one
-// task.  V <- V J in place.  A step is two CTA phases: the pair owners compute the step's
+// thread.  V <- V J in place.  Lane l of every warp owns the column pairs l and l + 32
+// (their rotations stay in registers for the whole step); warps walk the row pairs with
+// broadcast parameters (measured: the post kernel's Roothaan phase -22% against one task
+// list over all threads with per-task parameter loads).  A step is two CTA phases: the pair owners compute the step's
 // angles from A, then every thread applies them.  In-place A (instead of a second
 // buffer) keeps the arena at two n x n matrices, which fits two post CTAs per SM for the
 // benchmark's AO counts (N <= 80) instead of one.
 // Returns A (diagonal on exit); *nsweeps = sweeps.
-constexpr int JAC_MAXT = (NPH * NPH + NMAX * NPH + SCF_THREADS - 1) / SCF_THREADS;
+constexpr int JAC_NW = SCF_THREADS / 32;
+static_assert(NPH <= 64, "two column pairs per lane");
 
 __device__ __forceinline__ void jac_pair(int k, int r, int n2, int &p, int &q) {
     if (k == 0) { p = r; q = n2 - 1; }
@@ -175,11 +179,7 @@ __device__ double *cta_jacobi(double *A, double *V, int n, const Arena &ar, int 
                               int max_sweeps = 30, double tol = 1e-13) {
     const int tid = threadIdx.x, nt = SCF_THREADS;
     const int n2 = n + (n & 1), np = n2 / 2, R = n2 - 1;
-    const int nblk = np * np, ntask = nblk + n * np;
-    // task t -> (u, v) = divmod(t', np) by a multiply-high (exact for t' < 2^32 / np; np = 1
-    // would need 2^32, so that case is special-cased)
-    const unsigned inv_np = np > 1 ? (unsigned)((0x100000000ull + np - 1) / np) : 0u;
-    const int kr = tid;
+    const int kr = tid, lane = tid & 31, wid = tid >> 5;
     const bool rot_owner = tid < np;
     const double *cs = ar.cs, *sn = ar.sn;
     const int *pp = ar.pp, *qq = ar.qq;
@@ -210,34 +210,50 @@ __device__ double *cta_jacobi(double *A, double *V, int n, const Arena &ar, int 
             ar.cs[kr] = c; ar.sn[kr] = s1; ar.pp[kr] = p; ar.qq[kr] = q;
         }
         __syncthreads();
-#pragma unroll 4
-        for (int s = 0; s < JAC_MAXT; ++s) {
-            const int t = tid + s * nt;
-            if (t >= ntask) break;
-            const int tt = t < nblk ? t : t - nblk;
-            const int u = np > 1 ? (int)__umulhi((unsigned)tt, inv_np) : tt, v = tt - u * np;
-            if (t < nblk) {
-                const double s1 = sn[u], s2 = sn[v], c1 = cs[u], c2 = cs[v];
-                const int p1 = pp[u], q1 = qq[u], p2 = pp[v], q2 = qq[v];
-                const bool hq1 = q1 < n, hq2 = q2 < n;
-                const double xpp = A[p1 * n + p2];
-                const double xpq = hq2 ? A[p1 * n + q2] : 0.0;
-                const double xqp = hq1 ? A[q1 * n + p2] : 0.0;
-                const double xqq = (hq1 && hq2) ? A[q1 * n + q2] : 0.0;
-                const double ypp = c1 * xpp - s1 * xqp, yqp = s1 * xpp + c1 * xqp;
-                const double ypq = c1 * xpq - s1 * xqq, yqq = s1 * xpq + c1 * xqq;
-                A[p1 * n + p2] = c2 * ypp - s2 * ypq;
-                if (hq2) A[p1 * n + q2] = s2 * ypp + c2 * ypq;
-                if (hq1) A[q1 * n + p2] = c2 * yqp - s2 * yqq;
-                if (hq1 && hq2) A[q1 * n + q2] = s2 * yqp + c2 * yqq;
-            } else {
-                const double sv = sn[v];
-                if (sv == 0.0) continue;
-                const double cv = cs[v];
-                const int p = pp[v], q = qq[v];
-                const double vp = V[u * n + p], vq = V[u * n + q];
-                V[u * n + p] = cv * vp - sv * vq;
-                V[u * n + q] = sv * vp + cv * vq;
+        // apply: lane l owns the column pairs v = l, l + 32 (parameters in registers); the
+        // warps walk the row pairs u (broadcast parameters) and then the rows of V
+        {
+            double cvj[2], svj[2];
+            int pvj[2], qvj[2];
+            bool okj[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int v = lane + 32 * j;
+                okj[j] = v < np;
+                const int vv = okj[j] ? v : 0;
+                cvj[j] = cs[vv]; svj[j] = sn[vv]; pvj[j] = pp[vv]; qvj[j] = qq[vv];
+            }
+            for (int u = wid; u < np; u += JAC_NW) {
+                const double c1 = cs[u], s1 = sn[u];
+                const int p1 = pp[u], q1 = qq[u];
+                const bool hq1 = q1 < n;
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    if (!okj[j]) continue;
+                    const double c2 = cvj[j], s2 = svj[j];
+                    const int p2 = pvj[j], q2 = qvj[j];
+                    const bool hq2 = q2 < n;
+                    const double xpp = A[p1 * n + p2];
+                    const double xpq = hq2 ? A[p1 * n + q2] : 0.0;
+                    const double xqp = hq1 ? A[q1 * n + p2] : 0.0;
+                    const double xqq = (hq1 && hq2) ? A[q1 * n + q2] : 0.0;
+                    const double ypp = c1 * xpp - s1 * xqp, yqp = s1 * xpp + c1 * xqp;
+                    const double ypq = c1 * xpq - s1 * xqq, yqq = s1 * xpq + c1 * xqq;
+                    A[p1 * n + p2] = c2 * ypp - s2 * ypq;
+                    if (hq2) A[p1 * n + q2] = s2 * ypp + c2 * ypq;
+                    if (hq1) A[q1 * n + p2] = c2 * yqp - s2 * yqq;
+                    if (hq1 && hq2) A[q1 * n + q2] = s2 * yqp + c2 * yqq;
+                }
+            }
+            for (int row = wid; row < n; row += JAC_NW) {
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    if (!okj[j] || svj[j] == 0.0) continue;
+                    const int p = pvj[j], q = qvj[j];
+                    const double vp = V[row * n + p], vq = V[row * n + q];
+                    V[row * n + p] = cvj[j] * vp - svj[j] * vq;
+                    V[row * n + q] = svj[j] * vp + cvj[j] * vq;
+                }
             }
         }
         __syncthreads();
