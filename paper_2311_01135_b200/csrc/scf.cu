@@ -29,6 +29,7 @@ struct Arena {
     double *cf;         // [10]
     double *red;        // [32]
     double *scal;       // [16] scalars broadcast
+    long long *dbgp;    // JAC_PHASES builds: [2] angle / apply cycles (else null)
 };
 
 constexpr int NPH = NMAX / 2 + 1;
@@ -50,6 +51,7 @@ __device__ __forceinline__ Arena carve(unsigned char *base, int nm) {
     a.cf = p; p += 10;
     a.red = p; p += 32;
     a.scal = p; p += 16;
+    a.dbgp = nullptr;
     int *q = (int *)p;
     a.pp = q; q += 2 * NPH;
     a.qq = q; q += 2 * NPH;
@@ -147,7 +149,7 @@ __device__ void cta_gemm(double *C, int ldc, const double *A, int lda, bool tA, 
 // Cyclic Jacobi, round-robin (circle) pairing: n/2 disjoint rotations per step,
 // applied at once as J^T A J on 2x2 blocks (rows of pair k1 x columns of pair k2), in
 // place: the blocks partition A, so every element is read and written by exactly one
-// thread.  V <- V J in place.  Lane l of every warp owns the column pairs l and l + 32
+// thread.  V <- V J in place, V stored transposed (V^T, eigenvector k in row k).  Lane l of every warp owns the column pairs l and l + 32
 // (their rotations stay in registers for the whole step); warps walk the row pairs with
 // broadcast parameters (measured: the post kernel's Roothaan phase -22% against one task
 // list over all threads with per-task parameter loads).  A step is two CTA phases: the pair owners compute the step's
@@ -164,13 +166,16 @@ __device__ __forceinline__ void jac_pair(int k, int r, int n2, int &p, int &q) {
     if (p > q) { int t = p; p = q; q = t; }
 }
 
+// tan of the annihilating angle, t = sign(y) x / (|y| + sqrt(y^2 + x^2)) with y = aqq - app,
+// x = 2 apq (= sign(th) / (|th| + sqrt(th^2 + 1)), th = y / x, with one division instead of
+// two: the angle step is a serial f64 chain that the whole CTA waits for)
 __device__ __forceinline__ void jac_angle(double app, double aqq, double apq, double &c, double &s) {
     c = 1.0;
     s = 0.0;
     if (fabs(apq) > 1e-300 && fabs(apq) > 1e-17 * (fabs(app) + fabs(aqq))) {
-        const double th = (aqq - app) / (2.0 * apq);
-        const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
-        c = rsqrt(t * t + 1.0);
+        const double y = aqq - app, x = 2.0 * apq;
+        const double t = (y >= 0.0 ? x : -x) / (fabs(y) + sqrt(fma(y, y, x * x)));
+        c = rsqrt(fma(t, t, 1.0));
         s = t * c;
     }
 }
@@ -202,6 +207,9 @@ __device__ double *cta_jacobi(double *A, double *V, int n, const Arena &ar, int 
             if (off <= tol * dg || off < 1e-300 || sweeps >= max_sweeps) break;
             ++sweeps;
         }
+#ifdef JAC_PHASES
+        long long jt0 = clock64();
+#endif
         if (rot_owner) {   // this step's angles from the current A
             int p, q;
             jac_pair(kr, r, n2, p, q);
@@ -210,6 +218,9 @@ __device__ double *cta_jacobi(double *A, double *V, int n, const Arena &ar, int 
             ar.cs[kr] = c; ar.sn[kr] = s1; ar.pp[kr] = p; ar.qq[kr] = q;
         }
         __syncthreads();
+#ifdef JAC_PHASES
+        long long jt1 = clock64();
+#endif
         // apply: lane l owns the column pairs v = l, l + 32 (parameters in registers); the
         // warps walk the row pairs u (broadcast parameters) and then the rows of V
         {
@@ -245,18 +256,24 @@ __device__ double *cta_jacobi(double *A, double *V, int n, const Arena &ar, int 
                     if (hq1 && hq2) A[q1 * n + q2] = s2 * yqp + c2 * yqq;
                 }
             }
-            for (int row = wid; row < n; row += JAC_NW) {
-#pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    if (!okj[j] || svj[j] == 0.0) continue;
-                    const int p = pvj[j], q = qvj[j];
-                    const double vp = V[row * n + p], vq = V[row * n + q];
-                    V[row * n + p] = cvj[j] * vp - svj[j] * vq;
-                    V[row * n + q] = svj[j] * vp + cvj[j] * vq;
+            // V is stored transposed (row k = eigenvector k): rotating eigenvectors p, q is a
+            // contiguous, conflict-free row operation; one warp per pair, lanes over components
+            for (int k = wid; k < np; k += JAC_NW) {
+                const double sv = sn[k];
+                if (sv == 0.0) continue;
+                const double cv = cs[k];
+                double *vp_row = V + pp[k] * n, *vq_row = V + qq[k] * n;
+                for (int row = lane; row < n; row += 32) {
+                    const double vp = vp_row[row], vq = vq_row[row];
+                    vp_row[row] = cv * vp - sv * vq;
+                    vq_row[row] = sv * vp + cv * vq;
                 }
             }
         }
         __syncthreads();
+#ifdef JAC_PHASES
+        if (tid == 0 && ar.dbgp) { ar.dbgp[0] += jt1 - jt0; ar.dbgp[1] += clock64() - jt1; }
+#endif
     }
     *nsweeps = sweeps;
     return A;
@@ -318,7 +335,7 @@ __global__ void __launch_bounds__(SCF_THREADS, 2) k_orth(DevBatch b, int nm) {
     for (int t = tid; t < N * N; t += SCF_THREADS) {
         const int row = t / N, i = t % N;  // eigenvector column i
         const int r = ar.perm[i] - (N - M);
-        if (r >= 0) b.X[o + (int64_t)row * N + r] = ar.B[row * N + i] / sqrt(ar.dv[i]);
+        if (r >= 0) b.X[o + (int64_t)row * N + r] = ar.B[i * N + row] / sqrt(ar.dv[i]);   // V^T
     }
     for (int t = tid; t < N * N; t += SCF_THREADS) {
         const int r = t % N;
@@ -514,9 +531,12 @@ __device__ void diis_extrapolate(const DevBatch &b, int m, int N, const double *
 
 __global__ void __launch_bounds__(SCF_THREADS, 2) k_post(DevBatch b, PostArgs pa) {
     extern __shared__ __align__(16) unsigned char ssm[];
-    const Arena ar = carve(ssm, pa.nm);
+    Arena ar = carve(ssm, pa.nm);
     const int m = b.mol_order[blockIdx.x], tid = threadIdx.x;
     if (b.done[m]) return;
+#ifdef JAC_PHASES
+    if (b.dbg) ar.dbgp = b.dbg + 16 * m + 14;   // dbg[14], dbg[15]: Jacobi angle / apply cycles
+#endif
     const int N = b.m_nao[m], M = b.nmo[m], nocc = b.m_nocc[m];
     if (b.status[m] & (DFTB_ST_OVERLAP_NOT_PD | DFTB_ST_NO_ORBITALS)) {
         if (tid == 0) b.done[m] = 1;
@@ -608,7 +628,7 @@ __global__ void __launch_bounds__(SCF_THREADS, 2) k_post(DevBatch b, PostArgs pa
         // warm start: Jacobi on C'^T F' C' with V = C' (previous eigenvectors)
         cta_gemm(S1, M, ar.A, M, false, Cp, M, false, M, M, M, 1.0, 0.0, ar); // F' C'
         cta_gemm(ar.A, M, Cp, M, true, S1, M, false, M, M, M, 1.0, 0.0, ar);  // C'^T F' C'
-        for (int t = tid; t < M * M; t += SCF_THREADS) ar.B[t] = Cp[t];
+        for (int t = tid; t < M * M; t += SCF_THREADS) ar.B[(t % M) * M + t / M] = Cp[t];   // V^T = C'^T
     } else {
         for (int t = tid; t < M * M; t += SCF_THREADS) ar.B[t] = (t / M == t % M) ? 1.0 : 0.0;
     }
@@ -625,7 +645,7 @@ __global__ void __launch_bounds__(SCF_THREADS, 2) k_post(DevBatch b, PostArgs pa
     tick(5);
     for (int t = tid; t < M * M; t += SCF_THREADS) {
         const int row = t / M, i = t % M;
-        Cp[row * M + ar.perm[i]] = ar.B[t];
+        Cp[row * M + ar.perm[i]] = ar.B[i * M + row];
     }
     for (int i = tid; i < M; i += SCF_THREADS) b.eps[(int64_t)m * NMAX + ar.perm[i]] = ar.dv[i];
     __syncthreads();
@@ -696,7 +716,7 @@ __global__ void __launch_bounds__(SCF_THREADS) k_roothaan(DevBatch b, int nm) {
     int nsw = 0;
     const double *Ad = cta_jacobi(ar.A, ar.B, M, ar, &nsw);
     sort_eigs(Ad, M, ar);
-    for (int t = tid; t < M * M; t += SCF_THREADS) Cp[(t / M) * M + ar.perm[t % M]] = ar.B[t];
+    for (int t = tid; t < M * M; t += SCF_THREADS) Cp[(t / M) * M + ar.perm[t % M]] = ar.B[(t % M) * M + t / M];
     for (int i = tid; i < M; i += SCF_THREADS) b.eps[(int64_t)m * NMAX + ar.perm[i]] = ar.dv[i];
     __syncthreads();
     cta_gemm(C, N, X, N, false, Cp, M, false, N, M, M, 1.0, 0.0, ar);

@@ -12,4 +12,4 @@ for prec in ("f32", "f64"):
             d = p.get("dbg", m)
             print(prec, "mol", m, "N", p.pk.mol_nao[m], "post phases (Mcycles, summed over calls):",
                   [round(x / 1e6, 3) for x in d[:7]], "jacobi sweeps total", d[10], "calls", d[11],
-                  "orth cycles %.3fM sweeps %d" % (d[12] / 1e6, d[13]))
+                  "orth cycles %.3fM sweeps %d" % (d[12] / 1e6, d[13]), "jacobi angle/apply Mcycles %.3f %.3f" % (d[14] / 1e6, d[15] / 1e6))
