@@ -8,6 +8,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -119,20 +123,58 @@ int dftb_device_count(int *count) {
     return 0;
 }
 
+// Per-device pool of {aux stream, fork event, join event}: plans take one at creation and
+// return it at destruction, never destroying it.  Creating and destroying streams / events per
+// plan blocked the pipeline's host threads for the duration of other batches' device work
+// (measured: plan creation stalled 152 ms in cudaStreamCreateWithFlags while another batch ran),
+// which cut the batches in flight of the public labeling path from 3 to ~1.
+struct AuxSet { cudaStream_t s; cudaEvent_t fork, join; };
+static std::mutex g_aux_mu;
+static std::vector<AuxSet> g_aux_free[64];
+
+static bool aux_take(int dev, AuxSet &a) {
+    {
+        std::lock_guard<std::mutex> lock(g_aux_mu);
+        auto &v = g_aux_free[dev & 63];
+        if (!v.empty()) {
+            a = v.back();
+            v.pop_back();
+            return true;
+        }
+    }
+    a = AuxSet{nullptr, nullptr, nullptr};
+    if (cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming) != cudaSuccess)
+        return false;
+    return true;
+}
+static void aux_give(int dev, const AuxSet &a) {
+    std::lock_guard<std::mutex> lock(g_aux_mu);
+    g_aux_free[dev & 63].push_back(a);
+}
+
 int dftb_plan_destroy(dftb_plan *p) {
     if (!p) return 0;
     if (p->aux) cudaStreamSynchronize(p->aux);
     if (p->mem) cudaFreeAsync(p->mem, p->stream);   // back to the retained stream-ordered pool
     for (auto &e : p->ev)
         if (e) cudaEventDestroy(e);
-    if (p->fork) cudaEventDestroy(p->fork);
-    if (p->join) cudaEventDestroy(p->join);
-    if (p->aux) cudaStreamDestroy(p->aux);
+    if (p->aux && p->fork && p->join) aux_give(p->device, AuxSet{p->aux, p->fork, p->join});
     delete p;
     return 0;
 }
 
+// QM1B_TRACE=1: host-time trace of plan creation phases (stderr)
+static double trace_ms() {
+    static const bool on = std::getenv("QM1B_TRACE") != nullptr;
+    if (!on) return -1.0;
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+#define TRACE(label, t0) do { const double t_ = trace_ms(); if (t_ >= 0) { std::fprintf(stderr, "[qm1b] %s %.2f ms\n", label, t_ - (t0)); (t0) = t_; } } while (0)
+
 int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *stream, dftb_plan **out) {
+    double tr = trace_ms();
     if (!in || !opts || !out) return fail(DFTB_EINVAL, "null argument");
     if (opts->max_iterations < 1) return fail(DFTB_EINVAL, "max_iterations must be >= 1");
     if (opts->diis_history < 1 || opts->diis_history > DIIS_MAX) return fail(DFTB_EINVAL, "diis_history must be in 1..8");
@@ -409,14 +451,19 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
         }
         pool_set[p->device] = true;
     }
+    TRACE("plan", tr);
     p->stream = st;
-    if (cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&p->join, cudaEventDisableTiming) != cudaSuccess) {
-        dftb_plan_destroy(p);
-        return fail(DFTB_ECUDA, "stream/event creation failed");
+    {
+        AuxSet a;
+        if (!aux_take(p->device, a)) {
+            dftb_plan_destroy(p);
+            return fail(DFTB_ECUDA, "stream/event creation failed");
+        }
+        p->aux = a.s; p->fork = a.fork; p->join = a.join;
     }
+    TRACE("streams", tr);
     cudaError_t ce = cudaMallocAsync((void **)&p->mem, p->mem_bytes, st);
+    TRACE("malloc", tr);
     if (ce != cudaSuccess) {
         p->mem = nullptr;
         dftb_plan_destroy(p);
@@ -427,7 +474,9 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
     for (auto &u : ups)
         if (u.bytes) std::memcpy(blob.data() + u.off, u.src, u.bytes);
     ce = cudaMemcpyAsync(p->mem, blob.data(), p->in_bytes, cudaMemcpyHostToDevice, st);
+    TRACE("copy", tr);
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);  // blob is pageable and local
+    TRACE("sync", tr);
     if (ce != cudaSuccess) {
         dftb_plan_destroy(p);
         return fail(DFTB_ECUDA, std::string("upload: ") + cudaGetErrorString(ce));
@@ -760,7 +809,8 @@ int dftb_plan_xc(dftb_plan *p, const double *rho_host, double *Vxc_host, double 
     CK(cudaStreamSynchronize(st));
     int bad = 0;
     std::vector<int> status(p->d.n_mol);
-    CK(cudaMemcpy(status.data(), p->d.status, sizeof(int) * p->d.n_mol, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(status.data(), p->d.status, sizeof(int) * p->d.n_mol, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
     for (int s : status) bad |= s & DFTB_ST_XC_NONFINITE;
     if (bad) return fail(DFTB_ENUMERIC, "non-finite functional output (density underflow mishandled)");
     return 0;
