@@ -76,16 +76,20 @@ struct XCL {
     static constexpr size_t fpt = red + sizeof(double) * 32;      // functional parts [10][BP]
     static constexpr size_t dw = fpt + sizeof(double) * 10 * BP;  // wv coefficients [4][BP] (W)
     static constexpr size_t shd = dw + ((sizeof(W) * 4 * BP + 15) & ~(size_t)15);
-    static size_t bytes(int nsh) { return shd + sizeof(double) * XC_SHD * (size_t)nsh; }
+    // shell records: centres [nsh][3] f64 (for the point - centre difference), exponents and
+    // coefficients [nsh][9] in W (no per-use f64 -> f32 conversions), (ao << 1 | kind) [nsh]
+    static size_t bytes(int nsh) { return shd + (3 * sizeof(double) + 9 * sizeof(W) + sizeof(int)) * (size_t)nsh; }
 };
 
 template <typename W, int NQ, int BP>
-__device__ __forceinline__ void xc_eval_phi(W *phi, const double *pt, const double *shd, int nsh, int nb) {
+__device__ __forceinline__ void xc_eval_phi(W *phi, const double *pt, const double *shd, const W *shw,
+                                            const int *shi, int nsh, int nb) {
     constexpr int NP = 4 * NQ, PL = NP * BP;
     for (int t = threadIdx.x; t < BP * nsh; t += XC_THREADS) {
         const int p = t % BP, sh = t / BP;
-        const double *r = shd + XC_SHD * sh;
-        const int kind = (int)r[12] & 1, ao = (int)r[12] >> 1;
+        const double *r = shd + 3 * sh;
+        const W *f = shw + 9 * sh;
+        const int kind = shi[sh] & 1, ao = shi[sh] >> 1;
         W v[4][4];  // [plane][component]
 #pragma unroll
         for (int a = 0; a < 4; ++a)
@@ -98,16 +102,16 @@ __device__ __forceinline__ void xc_eval_phi(W *phi, const double *pt, const doub
             W bs = 0, ds = 0, bp = 0, dp = 0;
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                const W a = (W)r[3 + k];
+                const W a = f[k];
                 const W ar = a * r2;
                 W e;
                 if constexpr (sizeof(W) == 4) e = ar < (W)88 ? expf(-ar) : (W)0;
                 else e = ar < (W)745 ? exp(-ar) : (W)0;
                 const W m2a = (W)-2 * a;
-                bs += (W)r[6 + k] * e;
-                ds += (W)r[6 + k] * m2a * e;
-                bp += (W)r[9 + k] * e;
-                dp += (W)r[9 + k] * m2a * e;
+                bs += f[3 + k] * e;
+                ds += f[3 + k] * m2a * e;
+                bp += f[6 + k] * e;
+                dp += f[6 + k] * m2a * e;
             }
             const W rel[3] = {dx, dy, dz};
             v[0][0] = bs;
@@ -120,8 +124,9 @@ __device__ __forceinline__ void xc_eval_phi(W *phi, const double *pt, const doub
                 for (int d = 0; d < 3; ++d) v[d + 1][1 + c] = (c == d ? bp : (W)0) + rel[c] * rel[d] * dp;
             }
         }
-        const int nc = kind ? 4 : 1;
-        for (int c = 0; c < nc; ++c) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {   // fully unrolled: v stays in registers
+            if (c > 0 && !kind) break;
             const int o = swz<BP>(ao + c, p);
 #pragma unroll
             for (int a = 0; a < 4; ++a) phi[a * PL + o] = v[a][c];
@@ -130,7 +135,7 @@ __device__ __forceinline__ void xc_eval_phi(W *phi, const double *pt, const doub
 }
 
 template <typename W, int NQ, int BP>
-__global__ void __launch_bounds__(XC_THREADS) k_xc(DevBatch b, const int *ctas) {
+__global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *ctas) {
     using L = XCL<W, NQ, BP>;
     constexpr int NP = 4 * NQ, PL = NP * BP;
     constexpr int PG = BP / 4;                 // point groups (4 points each)
@@ -153,6 +158,8 @@ __global__ void __launch_bounds__(XC_THREADS) k_xc(DevBatch b, const int *ctas) 
     double *fpt = (double *)(xsm + L::fpt);
     W *dw = (W *)(xsm + L::dw);
     double *shd = (double *)(xsm + L::shd);
+    W *shw = (W *)(shd + 3 * nsh);
+    int *shi = (int *)(shw + 9 * nsh);
     const int tid = threadIdx.x;
     const double *rg = b.rho + b.m_mat0[m];
     for (int t = tid; t < NP * NP; t += XC_THREADS) {
@@ -162,15 +169,16 @@ __global__ void __launch_bounds__(XC_THREADS) k_xc(DevBatch b, const int *ctas) 
     for (int t = tid; t < 4 * PL; t += XC_THREADS) phi[t] = (W)0;
     for (int sh = tid; sh < nsh; sh += XC_THREADS) {
         const int gsh = s0 + sh;
-        double *r = shd + XC_SHD * sh;
+        double *r = shd + 3 * sh;
+        W *f = shw + 9 * sh;
         const double *A = b.a_xyz + 3 * b.s_atom[gsh];
         for (int d = 0; d < 3; ++d) {
             r[d] = A[d];
-            r[3 + d] = b.s_exp[3 * gsh + d];
-            r[6 + d] = b.s_cs[3 * gsh + d];
-            r[9 + d] = b.s_cp[3 * gsh + d];
+            f[d] = (W)b.s_exp[3 * gsh + d];
+            f[3 + d] = (W)b.s_cs[3 * gsh + d];
+            f[6 + d] = (W)b.s_cp[3 * gsh + d];
         }
-        r[12] = (double)((b.s_ao[gsh] << 1) | (b.s_kind[gsh] & 1));
+        shi[sh] = (b.s_ao[gsh] << 1) | (b.s_kind[gsh] & 1);
     }
     W acc[TJ][4][4];
 #pragma unroll
@@ -194,7 +202,7 @@ __global__ void __launch_bounds__(XC_THREADS) k_xc(DevBatch b, const int *ctas) 
             pt[4 * tid + 3] = tid < nb ? b.g_w[gi] : 0.0;
         }
         __syncthreads();
-        xc_eval_phi<W, NQ, BP>(phi, pt, shd, nsh, nb);
+        xc_eval_phi<W, NQ, BP>(phi, pt, shd, shw, shi, nsh, nb);
         __syncthreads();
         {   // ---- t = phi^T rho for 4 points x 4 AOs, then n and grad n partials
             W n4[4] = {0, 0, 0, 0}, g4[3][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}};
