@@ -217,6 +217,7 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
                         for (int c = 0; c < 4; ++c) t[a][c] = (W)0;
                     // k ascending in groups of 4 rows: the swizzled column of a 4-row group is
                     // one XOR (rows >= N are zero in phi and rho, so the tail adds exact zeros)
+#pragma unroll 2
                     for (int kq = 0; kq < (N + 3) / 4; ++kq) {
                         const W *pr = phi + 4 * kq * BP + (((pg ^ kq) & (BP / 4 - 1)) << 2);
                         const W *rr = rho + 4 * kq * NP + 4 * q;
@@ -313,11 +314,14 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
             }
         }
         __syncthreads();
-        for (int t = tid; t < PL; t += XC_THREADS) {       // ---- wv = a phi + b . grad phi
-            const int row = t / BP, p = t % BP;
-            const int o = swz<BP>(row, p);
-            wv[o] = dw[p] * phi[o] + dw[BP + p] * phi[PL + o] + dw[2 * BP + p] * phi[2 * PL + o] +
-                    dw[3 * BP + p] * phi[3 * PL + o];
+        {   // ---- wv = a phi + b . grad phi; this thread's point is fixed (XC_THREADS % BP == 0)
+            static_assert(XC_THREADS % BP == 0, "fixed point per thread");
+            const int p = tid % BP;
+            const W d0 = dw[p], d1 = dw[BP + p], d2 = dw[2 * BP + p], d3 = dw[3 * BP + p];
+            for (int row = tid / BP; row < NP; row += XC_THREADS / BP) {
+                const int o = swz<BP>(row, p);
+                wv[o] = d0 * phi[o] + d1 * phi[PL + o] + d2 * phi[2 * PL + o] + d3 * phi[3 * PL + o];
+            }
         }
         __syncthreads();
 #pragma unroll
