@@ -344,19 +344,23 @@ __global__ void __launch_bounds__(SCF_THREADS, 2) k_orth(DevBatch b, int nm) {
 }
 
 
+#ifndef SEQ_SUM_BATCH
+#define SEQ_SUM_BATCH 16
+#endif
 // sum_{u < n} load(u) accumulated left to right (bitwise the plain loop's result), with
 // the loads issued 8 at a time: the partial reductions below read L2/HBM, and a serial
 // load-add chain left them latency-bound (~20% of the post kernel).
 template <typename F>
 __device__ __forceinline__ double seq_sum(int n, F load) {
+    constexpr int B = SEQ_SUM_BATCH;
     double v = 0.0;
     int u = 0;
-    for (; u + 8 <= n; u += 8) {
-        double x[8];
+    for (; u + B <= n; u += B) {
+        double x[B];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) x[k] = load(u + k);
+        for (int k = 0; k < B; ++k) x[k] = load(u + k);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v += x[k];
+        for (int k = 0; k < B; ++k) v += x[k];
     }
     for (; u < n; ++u) v += load(u);
     return v;
