@@ -279,6 +279,60 @@ __device__ double *cta_jacobi(double *A, double *V, int n, const Arena &ar, int 
     return A;
 }
 
+// Eigenvalues of a small symmetric matrix (n <= 9: the bordered DIIS system) by the same
+// cyclic Jacobi as cta_jacobi (same pairing, angles and block updates, so A is bitwise the
+// same), run by warp 0 alone with warp barriers and without eigenvectors: the CTA-wide
+// version paid two CTA barriers per step for 25 block updates.  Callers __syncthreads after.
+__device__ void warp_jacobi_eigs(double *A, int n, const Arena &ar, double tol = 1e-13, int max_sweeps = 30) {
+    const int lane = threadIdx.x & 31;
+    const int n2 = n + (n & 1), np = n2 / 2, R = n2 - 1;
+    int sweeps = 0;
+    for (int g = 0;; ++g) {
+        const int r = g % R;
+        if (r == 0) {
+            double off = 0.0, dg = 0.0;
+            for (int t = lane; t < n * n; t += 32) {
+                const int p = t / n, q = t - p * n;
+                const double a = fabs(A[t]);
+                if (q > p) {
+                    if (a > 1e-15 * sqrt(fabs(A[p * n + p] * A[q * n + q]))) off = fmax(off, a);
+                } else if (q == p) {
+                    dg = fmax(dg, a);
+                }
+            }
+            off = warp_max(off);
+            dg = warp_max(dg);
+            if (off <= tol * dg || off < 1e-300 || sweeps >= max_sweeps) break;
+            ++sweeps;
+        }
+        if (lane < np) {
+            int p, q;
+            jac_pair(lane, r, n2, p, q);
+            double c = 1.0, s1 = 0.0;
+            if (q < n) jac_angle(A[p * n + p], A[q * n + q], A[p * n + q], c, s1);
+            ar.cs[lane] = c; ar.sn[lane] = s1; ar.pp[lane] = p; ar.qq[lane] = q;
+        }
+        __syncwarp();
+        if (lane < np * np) {
+            const int u = lane / np, v = lane % np;
+            const double s1 = ar.sn[u], s2 = ar.sn[v], c1 = ar.cs[u], c2 = ar.cs[v];
+            const int p1 = ar.pp[u], q1 = ar.qq[u], p2 = ar.pp[v], q2 = ar.qq[v];
+            const bool hq1 = q1 < n, hq2 = q2 < n;
+            const double xpp = A[p1 * n + p2];
+            const double xpq = hq2 ? A[p1 * n + q2] : 0.0;
+            const double xqp = hq1 ? A[q1 * n + p2] : 0.0;
+            const double xqq = (hq1 && hq2) ? A[q1 * n + q2] : 0.0;
+            const double ypp = c1 * xpp - s1 * xqp, yqp = s1 * xpp + c1 * xqp;
+            const double ypq = c1 * xpq - s1 * xqq, yqq = s1 * xpq + c1 * xqq;
+            A[p1 * n + p2] = c2 * ypp - s2 * ypq;
+            if (hq2) A[p1 * n + q2] = s2 * ypp + c2 * ypq;
+            if (hq1) A[q1 * n + p2] = c2 * yqp - s2 * yqq;
+            if (hq1 && hq2) A[q1 * n + q2] = s2 * yqp + c2 * yqq;
+        }
+        __syncwarp();
+    }
+}
+
 // ascending order of diag(A) -> ar.perm (rank of each original index), stable by index
 __device__ void sort_dv(int n, const Arena &ar);
 __device__ void sort_eigs(const double *A, int n, const Arena &ar) {
@@ -475,8 +529,8 @@ __device__ void diis_extrapolate(const DevBatch &b, int m, int N, const double *
         ar.B[t] = (r == c) ? 1.0 : 0.0;
     }
     __syncthreads();
-    int nsw1 = 0;
-    const double *Ad = cta_jacobi(ar.A, ar.B, n1, ar, &nsw1);
+    if (tid < 32) warp_jacobi_eigs(ar.A, n1, ar);
+    const double *Ad = ar.A;
     if (tid == 0) {
         double mx = 0.0, mn = 1e308;
         for (int i = 0; i < n1; ++i) {
@@ -763,8 +817,8 @@ __global__ void __launch_bounds__(SCF_THREADS) k_diis_single(const double *F, co
         ar.B[t] = (t / n1 == t % n1) ? 1.0 : 0.0;
     }
     __syncthreads();
-    int nsw2 = 0;
-    const double *Ad = cta_jacobi(ar.A, ar.B, n1, ar, &nsw2);
+    if (tid < 32) warp_jacobi_eigs(ar.A, n1, ar);
+    const double *Ad = ar.A;
     if (tid == 0) {
         double mx = 0.0, mn = 1e308;
         for (int i = 0; i < n1; ++i) { const double e = fabs(Ad[i * n1 + i]); mx = fmax(mx, e); mn = fmin(mn, e); }
