@@ -174,13 +174,20 @@ __global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, const int *ctas) 
         const int r = t / NP, c = t % NP;
         rho[rsw<NP>(r, c)] = (r < N && c < N) ? rg[r * N + c] : 0.0;
     }
+    // this CTA's exchange partial Kc (N x N, CTA-private): the rows G_j of its slabs are
+    // accumulated here instead of being stored one slab row at a time, so the post kernel
+    // reads ncta N^2 instead of tri(N) N.  The adds are fire-and-forget reductions (RED, no
+    // latency on the row's critical path); an element gets at most one add per chunk and the
+    // chunks are separated by CTA barriers, so the order of the adds - and the result - is
+    // fixed (deterministic, batch invariant).
+    double *Gp = b.Gpart + b.m_G0[m] + (int64_t)(cta - b.m_jkcta0[m]) * N * N;
+    for (int t = tid; t < N * N; t += JK_THREADS) Gp[t] = 0.0;
     __syncthreads();
     double acc[KU][VW];
 #pragma unroll
     for (int k = 0; k < KU; ++k)
 #pragma unroll
         for (int v = 0; v < VW; ++v) acc[k][v] = 0.0;
-    double *Gp = b.Gpart + b.m_G0[m];
     double *Jp = b.Jpart + b.m_Jp0[m];
     int chunk = 0;
     for (int i = i1 - 1; i >= i0; --i) {
@@ -276,14 +283,14 @@ __global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, const int *ctas) 
                 const double rjI = rho[rsw<NP>(j, i)], rjJ = rho[rsw<NP>(j, j)];
                 const double riI = rho[rsw<NP>(i, i)], riJ = rho[rsw<NP>(i, j)];
                 if (lane_ok && s == 0) {
-                    double *Gj = Gp + (tri(i) + j) * N;
+                    double *Gj = Gp + (int64_t)j * N;
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         const int t = 4 * a + u;
                         double gJ = 2.0 * oI[u];
                         if (t == j) { gi[u] -= vp * rjI; gJ -= vp * riI; }
                         else if (t == i) { gi[u] -= vp * rjJ; gJ -= vp * riJ; }
-                        if (j < i && t <= i) Gj[t] = gJ;
+                        if (j < i && t <= i) atomicAdd(Gj + t, gJ);   // RED, see Kc above
                     }
                 }
                 if (lane == 0) Jp[tri(i) + j] = 2.0 * jp - vp * riJ * (i != j ? 2.0 : 1.0);
@@ -323,13 +330,13 @@ __global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, const int *ctas) 
         for (int u = 0; u < 4; ++u) gred[tid * 4 + u] = gi[u];
         __syncthreads();
         if (tid < A) {                                 // thread tid handles block tid
-            double *Gi = Gp + (tri(i) + i) * N;
+            double *Gi = Gp + (int64_t)i * N;
             for (int u = 0; u < 4; ++u) {
                 const int t = 4 * tid + u;
                 if (t > i) break;
                 double v = 0.0;
                 for (int ww = 0; ww < CR; ++ww) v += gred[(ww * 32 + tid * S) * 4 + u];
-                Gi[t] = v;
+                atomicAdd(Gi + t, v);
             }
         }
         __syncthreads();

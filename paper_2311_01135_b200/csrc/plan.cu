@@ -266,7 +266,6 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
         p->mat0[m + 1] = p->mat0[m] + N * N;
         p->npp0[m + 1] = p->npp0[m] + npp;
         eri0[m + 1] = eri0[m] + eri_size((int)N);
-        G0[m + 1] = G0[m] + N * (N + 1) / 2 * N;
         // J/K CTAs: contiguous whole-slab ranges [i0, i1) of about equal tile-row work
         // (slab i = the i + 1 store rows (i, j); its work is (i + 1) * tri(i/4 + 1) tiles)
         int ncj = 0;
@@ -293,6 +292,7 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
             jk_mol.push_back(m); jk_i0.push_back(0); jk_i1.push_back(hi); ++ncj;
         }
         p->jkc0[m + 1] = p->jkc0[m] + ncj;
+        G0[m + 1] = G0[m] + (int64_t)ncj * N * N;      // one N x N exchange partial per J/K CTA
         Jp0[m + 1] = Jp0[m] + (int64_t)(ncj + 1) * npp;
         p->grid0[m] = a_grid0[atom0[m]];
         const int64_t g_end = a_grid0[atom0[m + 1]];

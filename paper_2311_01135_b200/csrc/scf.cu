@@ -435,12 +435,9 @@ __device__ void reduce_jk(const DevBatch &b, int m, int N, double *J, double *K)
         J[k * N + l] = v;
         J[l * N + k] = v;
     }
-    const double *Gp = b.Gpart + b.m_G0[m];
-    for (int t = tid; t < N * N; t += SCF_THREADS) {
-        const int a = t / N, c = t % N;
-        const int i0 = max(a, c);
-        K[t] = seq_sum(N - i0, [&](int u) { return Gp[(tri(i0 + u) + a) * N + c]; });
-    }
+    const double *Gp = b.Gpart + b.m_G0[m];   // [ncj][N][N] per-CTA exchange partials
+    const int64_t NN = (int64_t)N * N;
+    for (int t = tid; t < N * N; t += SCF_THREADS) K[t] = seq_sum(ncj, [&](int c) { return Gp[c * NN + t]; });
     __syncthreads();
     for (int t = tid; t < N * N; t += SCF_THREADS) {
         const int a = t / N, c = t % N;
