@@ -162,6 +162,26 @@ __device__ __forceinline__ double block_sum(double v, double *red) {
     __syncthreads();
     return t;
 }
+// two block maxima with one set of barriers (red: >= 64 doubles)
+__device__ __forceinline__ void block_max2(double &a, double &b, double *red) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    a = warp_max(a);
+    b = warp_max(b);
+    __syncthreads();
+    if (lane == 0) { red[w] = a; red[32 + w] = b; }
+    __syncthreads();
+    if (w == 0) {
+        double x = lane < nw ? red[lane] : 0.0, y = lane < nw ? red[32 + lane] : 0.0;
+        x = warp_max(x);
+        y = warp_max(y);
+        if (lane == 0) { red[0] = x; red[32] = y; }
+    }
+    __syncthreads();
+    a = red[0];
+    b = red[32];
+    __syncthreads();
+}
+
 __device__ __forceinline__ double block_max(double v, double *red) {
     int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
     v = warp_max(v);

@@ -27,7 +27,7 @@ struct Arena {
     double *dv;         // [NMAX]
     double *Bs;         // [10*10] DIIS system
     double *cf;         // [10]
-    double *red;        // [32]
+    double *red;        // [64]
     double *scal;       // [16] scalars broadcast
     long long *dbgp;    // JAC_PHASES builds: [2] angle / apply cycles (else null)
 };
@@ -49,7 +49,7 @@ __device__ __forceinline__ Arena carve(unsigned char *base, int nm) {
     a.dv = p; p += NMAX;
     a.Bs = p; p += 100;
     a.cf = p; p += 10;
-    a.red = p; p += 32;
+    a.red = p; p += 64;
     a.scal = p; p += 16;
     a.dbgp = nullptr;
     int *q = (int *)p;
@@ -60,7 +60,7 @@ __device__ __forceinline__ Arena carve(unsigned char *base, int nm) {
 }
 
 size_t scf_smem_bytes(int nm) {
-    return sizeof(double) * ((size_t)nm * nm + arena_b(nm) + 4 * NPH + NMAX + 100 + 10 + 32 + 16) +
+    return sizeof(double) * ((size_t)nm * nm + arena_b(nm) + 4 * NPH + NMAX + 100 + 10 + 64 + 16) +
            sizeof(int) * (4 * NPH + NMAX);
 }
 
@@ -191,19 +191,18 @@ __device__ double *cta_jacobi(double *A, double *V, int n, const Arena &ar, int 
     int sweeps = 0;
     for (int g = 0;; ++g) {
         const int r = g % R;
-        if (r == 0) {
+        if (r == 0) {   // convergence: off-diagonal max (elements above 1e-15 sqrt|a_pp a_qq|) vs diagonal max
             double off = 0.0, dg = 0.0;
             for (int t = tid; t < n * n; t += nt) {
                 const int p = t / n, q = t - p * n;
-                const double a = fabs(A[t]);
+                const double a = A[t];
                 if (q > p) {
-                    if (a > 1e-15 * sqrt(fabs(A[p * n + p] * A[q * n + q]))) off = fmax(off, a);
+                    if (a * a > 1e-30 * fabs(A[p * n + p] * A[q * n + q])) off = fmax(off, fabs(a));   // no sqrt
                 } else if (q == p) {
-                    dg = fmax(dg, a);
+                    dg = fmax(dg, fabs(a));
                 }
             }
-            off = block_max(off, ar.red);
-            dg = block_max(dg, ar.red);
+            block_max2(off, dg, ar.red);
             if (off <= tol * dg || off < 1e-300 || sweeps >= max_sweeps) break;
             ++sweeps;
         }
