@@ -87,8 +87,10 @@ struct dftb_plan {
 
 // ------------------------------------------------------------------ Boys table (per device)
 static double *g_boys[64] = {nullptr};
+static std::mutex g_boys_mu;   // plans are created from several host threads (pipeline workers)
 static int ensure_boys(int dev, const double **out) {
     if (dev < 0 || dev >= 64) return fail(DFTB_EINVAL, "device index out of range");
+    std::lock_guard<std::mutex> lock(g_boys_mu);
     if (!g_boys[dev]) {
         std::vector<double> tab(BOYS_NT * BOYS_NCOL);
         boys_table_host(tab.data());
@@ -442,14 +444,18 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
     // ---------------- allocate + upload
     // stream-ordered allocation from the device's default pool, retained across plans so a
     // stream of batches does not pay cudaMalloc/cudaFree each time
-    static bool pool_set[64] = {false};
-    if (!pool_set[p->device]) {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, p->device) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    {
+        static bool pool_set[64] = {false};
+        static std::mutex pool_mu;
+        std::lock_guard<std::mutex> pool_lock(pool_mu);
+        if (!pool_set[p->device]) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, p->device) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+            pool_set[p->device] = true;
         }
-        pool_set[p->device] = true;
     }
     TRACE("plan", tr);
     p->stream = st;
