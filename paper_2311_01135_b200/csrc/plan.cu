@@ -453,6 +453,11 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
             if (cudaDeviceGetDefaultMemPool(&pool, p->device) == cudaSuccess) {
                 uint64_t thr = UINT64_MAX;
                 cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+                // no reuse of a block freed on another stream by making this stream wait for
+                // that stream's pending work (the free of a batch still running elsewhere):
+                // concurrent plans take their own blocks (the pool keeps them all)
+                int no = 0;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
             }
             pool_set[p->device] = true;
         }
@@ -468,7 +473,10 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
         p->aux = a.s; p->fork = a.fork; p->join = a.join;
     }
     TRACE("streams", tr);
-    cudaError_t ce = cudaMallocAsync((void **)&p->mem, p->mem_bytes, st);
+    // allocation rounded up to 64 MiB so the pool's blocks are interchangeable between the
+    // slightly different batch sizes that follow each other through the pipeline
+    const size_t alloc_bytes = (p->mem_bytes + ((size_t)64 << 20) - 1) & ~(((size_t)64 << 20) - 1);
+    cudaError_t ce = cudaMallocAsync((void **)&p->mem, alloc_bytes, st);
     TRACE("malloc", tr);
     if (ce != cudaSuccess) {
         p->mem = nullptr;
