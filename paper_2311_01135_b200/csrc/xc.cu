@@ -99,14 +99,19 @@ __device__ __forceinline__ void xc_eval_phi(W *phi, const double *pt, const doub
             const double *q = pt + 4 * p;
             const W dx = (W)(q[0] - r[0]), dy = (W)(q[1] - r[1]), dz = (W)(q[2] - r[2]);
             const W r2 = dx * dx + dy * dy + dz * dz;
+            constexpr W kCut = sizeof(W) == 4 ? (W)88 : (W)745;
+            // unless every primitive underflows (exponents descend, f[2] is the smallest; the
+            // AO values and gradients then stay exactly zero, as the loop would give: core
+            // shells far from the sub-block's points)
+            if (f[2] * r2 < kCut) {
             W bs = 0, ds = 0, bp = 0, dp = 0;
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 const W a = f[k];
                 const W ar = a * r2;
                 W e;
-                if constexpr (sizeof(W) == 4) e = ar < (W)88 ? expf(-ar) : (W)0;
-                else e = ar < (W)745 ? exp(-ar) : (W)0;
+                if constexpr (sizeof(W) == 4) e = ar < kCut ? expf(-ar) : (W)0;
+                else e = ar < kCut ? exp(-ar) : (W)0;
                 const W m2a = (W)-2 * a;
                 bs += f[3 + k] * e;
                 ds += f[3 + k] * m2a * e;
@@ -122,6 +127,7 @@ __device__ __forceinline__ void xc_eval_phi(W *phi, const double *pt, const doub
                 v[0][1 + c] = rel[c] * bp;
 #pragma unroll
                 for (int d = 0; d < 3; ++d) v[d + 1][1 + c] = (c == d ? bp : (W)0) + rel[c] * rel[d] * dp;
+            }
             }
         }
 #pragma unroll
