@@ -186,13 +186,19 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
         }
         shi[sh] = (b.s_ao[gsh] << 1) | (b.s_kind[gsh] & 1);
     }
-    W acc[TJ][4][4];
+    // V accumulators: f32 keeps two partial sums (even / odd points of each 4-point chunk)
+    // so every update is one packed FFMA2; f64 one DFMA chain
+    using VA = typename std::conditional<sizeof(W) == 4, float2, double>::type;
+    VA acc[TJ][4][4];
 #pragma unroll
     for (int j = 0; j < TJ; ++j)
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) acc[j][a][c] = (W)0;
+            for (int c = 0; c < 4; ++c) {
+                if constexpr (sizeof(W) == 4) acc[j][a][c] = make_float2(0.f, 0.f);
+                else acc[j][a][c] = 0.0;
+            }
     double e_acc = 0.0;
     int bad = 0;
     const int pg = tid / LG, lg = tid % LG;
@@ -215,7 +221,62 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
 #pragma unroll
             for (int j = 0; j < QJ; ++j) {
                 const int q = lg + j * LG;
-                if (q < NQ) {
+                if constexpr (sizeof(W) == 4) {
+                    // f32: Blackwell packed FFMA2 (two FMAs per instruction; the same per-element
+                    // fma and order as the scalar code below): t2[h][c] = (t[2h][c], t[2h+1][c])
+                    if (q < NQ) {
+                        float2 t2[2][4];
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) t2[h][c] = make_float2(0.f, 0.f);
+#pragma unroll 2
+                        for (int kq = 0; kq < (N + 3) / 4; ++kq) {
+                            const W *pr = phi + 4 * kq * BP + (((pg ^ kq) & (BP / 4 - 1)) << 2);
+                            const W *rr = rho + 4 * kq * NP + 4 * q;
+#pragma unroll
+                            for (int r = 0; r < 4; ++r) {
+                                const float4 f = *reinterpret_cast<const float4 *>(pr + r * BP);
+                                const float4 r4 = *reinterpret_cast<const float4 *>(rr + r * NP);
+                                const float2 f01 = make_float2(f.x, f.y), f23 = make_float2(f.z, f.w);
+                                const float rc[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+                                for (int c = 0; c < 4; ++c) {
+                                    t2[0][c] = __ffma2_rn(f01, make_float2(rc[c], rc[c]), t2[0][c]);
+                                    t2[1][c] = __ffma2_rn(f23, make_float2(rc[c], rc[c]), t2[1][c]);
+                                }
+                            }
+                        }
+                        const int qo = 4 * q * BP + (((pg ^ q) & (BP / 4 - 1)) << 2);   // rows 4q..4q+3
+                        float2 n2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+                        float2 g2[3][2] = {{make_float2(0.f, 0.f), make_float2(0.f, 0.f)},
+                                           {make_float2(0.f, 0.f), make_float2(0.f, 0.f)},
+                                           {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}};
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            float4 fp[4];
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) fp[k] = *reinterpret_cast<const float4 *>(phi + k * PL + qo + c * BP);
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const float2 f0 = h ? make_float2(fp[0].z, fp[0].w) : make_float2(fp[0].x, fp[0].y);
+                                n2[h] = __ffma2_rn(t2[h][c], f0, n2[h]);
+#pragma unroll
+                                for (int d = 0; d < 3; ++d) {
+                                    const float2 fd = h ? make_float2(fp[d + 1].z, fp[d + 1].w)
+                                                        : make_float2(fp[d + 1].x, fp[d + 1].y);
+                                    g2[d][h] = __ffma2_rn(t2[h][c], fd, g2[d][h]);
+                                }
+                            }
+                        }
+                        n4[0] += n2[0].x; n4[1] += n2[0].y; n4[2] += n2[1].x; n4[3] += n2[1].y;
+#pragma unroll
+                        for (int d = 0; d < 3; ++d) {
+                            g4[d][0] += g2[d][0].x; g4[d][1] += g2[d][0].y;
+                            g4[d][2] += g2[d][1].x; g4[d][3] += g2[d][1].y;
+                        }
+                    }
+                } else if (q < NQ) {
                     W t[4][4];
 #pragma unroll
                     for (int a = 0; a < 4; ++a)
@@ -347,9 +408,17 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
 #pragma unroll
                     for (int a = 0; a < 4; ++a)
 #pragma unroll
-                        for (int c = 0; c < 4; ++c)
+                        for (int c = 0; c < 4; ++c) {
+                            if constexpr (sizeof(W) == 4) {
+                                acc[j][a][c] = __ffma2_rn(make_float2(fa[a][0], fa[a][1]),
+                                                          make_float2(fb[c][0], fb[c][1]), acc[j][a][c]);
+                                acc[j][a][c] = __ffma2_rn(make_float2(fa[a][2], fa[a][3]),
+                                                          make_float2(fb[c][2], fb[c][3]), acc[j][a][c]);
+                            } else {
 #pragma unroll
-                            for (int pp = 0; pp < 4; ++pp) acc[j][a][c] += fa[a][pp] * fb[c][pp];
+                                for (int pp = 0; pp < 4; ++pp) acc[j][a][c] += fa[a][pp] * fb[c][pp];
+                            }
+                        }
                 }
             }
         }
@@ -366,7 +435,10 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     const int mu = 4 * qa + a, nu = 4 * qb + c;
-                    if (mu < N && nu < N) Vp[mu * N + nu] = (double)acc[j][a][c];
+                    if (mu < N && nu < N) {
+                        if constexpr (sizeof(W) == 4) Vp[mu * N + nu] = (double)(acc[j][a][c].x + acc[j][a][c].y);
+                        else Vp[mu * N + nu] = acc[j][a][c];
+                    }
                 }
         }
     }
