@@ -319,3 +319,26 @@ def test_config5_shape_level3_convergence(gpu_lib, sto3g):
         assert r.converged and r.iterations <= 50
         assert np.std(r.energy_history[-5:]) < 1e-9
     assert alone.E_total == batch[2].E_total and alone.iterations == batch[2].iterations
+
+
+@pytest.mark.slow
+def test_config5_level3_against_reference(gpu_lib, sto3g):
+    """BASELINE configs[4] settings (11 heavy atoms, f64, grid level 3, converged to
+    std(last 5 E) < 1e-9, max 50 iterations) against records produced by the reference
+    deskdft itself (tests/golden/make_golden_level3.py): total energy within 1e-6 Ha (the
+    fp64 bar), gap within 1e-5 eV, same iteration count."""
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(__file__), "golden", "level3.json")
+    if not os.path.exists(path):
+        pytest.skip("level-3 reference records not generated")
+    g = json.load(open(path))
+    mols = [Molecule(tuple(r["Z"]), np.asarray(r["pos_bohr"])) for r in g["molecules"]]
+    opts = SCFOptions(**g["options"])
+    res = scf_batch(mols, sto3g, opts)
+    for r, ref in zip(res, g["molecules"]):
+        assert abs(r.E_total - ref["E_total"]) < 1e-6, (r.E_total, ref["E_total"])
+        assert abs(properties(r)["gap"] - ref["gap_ev"]) < 1e-5
+        assert r.converged == ref["converged"]
+        assert r.iterations == ref["iterations"]
