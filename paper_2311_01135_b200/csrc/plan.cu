@@ -232,6 +232,37 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
                     ++cnt;
                 }
             npl[3 * m + cls] = cnt;
+#ifndef PAIR_SORT
+#define PAIR_SORT 1
+#endif
+            if (PAIR_SORT && cnt > 1) {
+                // order the class list by how slowly the pair's overlap decays: mu_min R^2 with
+                // mu_min the smallest alpha beta / (alpha + beta) of its primitive pairs (a
+                // geometric stand-in for the Schwarz bound), ascending.  The ERI kernels run 32
+                // consecutive kets per warp; kets of similar extent share their primitive screens
+                // and Schwarz outcome.  Stable, so the order is deterministic.
+                const size_t beg = p_sa.size() - (size_t)cnt;
+                std::vector<std::pair<double, int>> key((size_t)cnt);
+                for (int k = 0; k < cnt; ++k) {
+                    const int x = p_sa[beg + k], y = p_sb[beg + k];
+                    const double *A = in->atom_xyz + 3 * (size_t)(atom0[m] + in->shell_atom[x]);
+                    const double *B = in->atom_xyz + 3 * (size_t)(atom0[m] + in->shell_atom[y]);
+                    const double r2 = (A[0] - B[0]) * (A[0] - B[0]) + (A[1] - B[1]) * (A[1] - B[1]) +
+                                      (A[2] - B[2]) * (A[2] - B[2]);
+                    double mu = 1e300;
+                    for (int i = 0; i < 3; ++i)
+                        for (int j = 0; j < 3; ++j) {
+                            const double al = in->shell_exp[3 * x + i], be = in->shell_exp[3 * y + j];
+                            mu = std::min(mu, al * be / (al + be));
+                        }
+                    key[k] = {mu * r2, k};
+                }
+                std::stable_sort(key.begin(), key.end(),
+                                 [](const std::pair<double, int> &u, const std::pair<double, int> &v) { return u.first < v.first; });
+                std::vector<int> sa((size_t)cnt), sb((size_t)cnt);
+                for (int k = 0; k < cnt; ++k) { sa[k] = p_sa[beg + key[k].second]; sb[k] = p_sb[beg + key[k].second]; }
+                for (int k = 0; k < cnt; ++k) { p_sa[beg + k] = sa[k]; p_sb[beg + k] = sb[k]; }
+            }
         }
     }
     pair0[nm] = (int)p_sa.size();
