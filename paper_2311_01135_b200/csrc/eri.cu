@@ -307,6 +307,40 @@ static void launch_cls(const DevBatch &b, int cls, int64_t n, double eps, double
 #ifndef ERI_LSLS_NS
 #define ERI_LSLS_NS 6
 #endif
+// Registers vs resident warps per class (B200, 256 x 9-heavy batch): the kernels are
+// latency-bound, so more CTAs per SM pays even with some spills.  LL|LL at 3 CTAs (168
+// registers): 5.65 -> 5.29 ms; LL|LS at 4 CTAs (128 registers, 6-slot ket cache): 10.97 ->
+// 9.51 ms.
+#ifndef ERI_LLLL_MINB
+#define ERI_LLLL_MINB 3
+#endif
+#ifndef ERI_LLLL_NS
+#define ERI_LLLL_NS 7
+#endif
+#ifndef ERI_LLLS_MINB
+#define ERI_LLLS_MINB 4
+#endif
+#ifndef ERI_LLLS_NS
+#define ERI_LLLS_NS 6
+#endif
+#ifndef ERI_LLSS_KSM
+#define ERI_LLSS_KSM true
+#endif
+#ifndef ERI_LLSS_MINB
+#define ERI_LLSS_MINB ERI_S_MINB
+#endif
+#ifndef ERI_LSLS_KSM
+#define ERI_LSLS_KSM true
+#endif
+#ifndef ERI_LSSS_KSM
+#define ERI_LSSS_KSM false     // LS|SS: no ket cache, 8 CTAs/SM (64 registers): 13.0 -> 12.2 ms
+#endif
+#ifndef ERI_LSSS_MINB
+#define ERI_LSSS_MINB 8
+#endif
+#ifndef ERI_SSSS_MINB
+#define ERI_SSSS_MINB 12      // SS|SS: 12 CTAs/SM by registers (40): 5.61 -> 5.10 ms
+#endif
 #ifndef ERI_KPS_LL
 #define ERI_KPS_LL 2       // LL|LL: 8 slices of 2 ket components
 #endif
@@ -317,12 +351,12 @@ static void launch_cls(const DevBatch &b, int cls, int64_t n, double eps, double
 template <typename ST>
 static void launch_eri_t(const DevBatch &b, const int64_t *tot, double eps, double prim_cut,
                          ST *eri, cudaStream_t s, int *nlaunch) {
-    launch_cls<1, 1, 1, 1, ERI_KPS_LL>(b, 0, tot[0], eps, prim_cut, eri, s, nlaunch);
-    launch_cls<1, 1, 1, 0, ERI_KPS_LS>(b, 1, tot[1], eps, prim_cut, eri, s, nlaunch);
-    launch_cls<1, 1, 0, 0, 0, true, ERI_S_MINB>(b, 2, tot[2], eps, prim_cut, eri, s, nlaunch);
-    launch_cls<1, 0, 1, 0, 0, true, ERI_LSLS_MINB, ERI_LSLS_NS>(b, 3, tot[3], eps, prim_cut, eri, s, nlaunch);
-    launch_cls<1, 0, 0, 0, 0, true, ERI_S_MINB>(b, 4, tot[4], eps, prim_cut, eri, s, nlaunch);
-    launch_cls<0, 0, 0, 0, 0, false>(b, 5, tot[5], eps, prim_cut, eri, s, nlaunch);
+    launch_cls<1, 1, 1, 1, ERI_KPS_LL, true, ERI_LLLL_MINB, ERI_LLLL_NS>(b, 0, tot[0], eps, prim_cut, eri, s, nlaunch);
+    launch_cls<1, 1, 1, 0, ERI_KPS_LS, true, ERI_LLLS_MINB, ERI_LLLS_NS>(b, 1, tot[1], eps, prim_cut, eri, s, nlaunch);
+    launch_cls<1, 1, 0, 0, 0, ERI_LLSS_KSM, ERI_LLSS_MINB>(b, 2, tot[2], eps, prim_cut, eri, s, nlaunch);
+    launch_cls<1, 0, 1, 0, 0, ERI_LSLS_KSM, ERI_LSLS_MINB, ERI_LSLS_NS>(b, 3, tot[3], eps, prim_cut, eri, s, nlaunch);
+    launch_cls<1, 0, 0, 0, 0, ERI_LSSS_KSM, ERI_LSSS_MINB>(b, 4, tot[4], eps, prim_cut, eri, s, nlaunch);
+    launch_cls<0, 0, 0, 0, 0, false, ERI_SSSS_MINB>(b, 5, tot[5], eps, prim_cut, eri, s, nlaunch);
 }
 
 void launch_eri(const DevBatch &b, const int64_t *tot, double eps, double prim_cut, cudaStream_t s,
