@@ -83,6 +83,8 @@ struct dftb_plan {
     cudaStream_t stream = nullptr;
     cudaStream_t aux = nullptr;     // J/K runs here, concurrently with XC on the caller's stream
     cudaEvent_t fork = nullptr, join = nullptr;
+    cudaEvent_t fin = nullptr;      // this plan's last work on the caller's stream (fetch / free wait on it)
+    bool fin_rec = false;
 };
 
 // ------------------------------------------------------------------ Boys table (per device)
@@ -130,7 +132,7 @@ int dftb_device_count(int *count) {
 // plan blocked the pipeline's host threads for the duration of other batches' device work
 // (measured: plan creation stalled 152 ms in cudaStreamCreateWithFlags while another batch ran),
 // which cut the batches in flight of the public labeling path from 3 to ~1.
-struct AuxSet { cudaStream_t s; cudaEvent_t fork, join; };
+struct AuxSet { cudaStream_t s; cudaEvent_t fork, join, fin; };
 static std::mutex g_aux_mu;
 static std::vector<AuxSet> g_aux_free[64];
 
@@ -144,10 +146,11 @@ static bool aux_take(int dev, AuxSet &a) {
             return true;
         }
     }
-    a = AuxSet{nullptr, nullptr, nullptr};
+    a = AuxSet{nullptr, nullptr, nullptr, nullptr};
     if (cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&a.fin, cudaEventDisableTiming) != cudaSuccess)
         return false;
     return true;
 }
@@ -158,11 +161,17 @@ static void aux_give(int dev, const AuxSet &a) {
 
 int dftb_plan_destroy(dftb_plan *p) {
     if (!p) return 0;
+    // the free is ordered after this plan's last submitted work (fin) on the aux stream, not
+    // after whatever the caller's stream holds by now (the pipeline queues the next batch there)
+    if (p->aux && p->fin) {
+        if (!p->fin_rec && p->stream) cudaEventRecord(p->fin, p->stream);   // no run: all of st so far
+        cudaStreamWaitEvent(p->aux, p->fin, 0);
+    }
+    if (p->mem) cudaFreeAsync(p->mem, p->aux ? p->aux : p->stream);   // back to the retained pool
     if (p->aux) cudaStreamSynchronize(p->aux);
-    if (p->mem) cudaFreeAsync(p->mem, p->stream);   // back to the retained stream-ordered pool
     for (auto &e : p->ev)
         if (e) cudaEventDestroy(e);
-    if (p->aux && p->fork && p->join) aux_give(p->device, AuxSet{p->aux, p->fork, p->join});
+    if (p->aux && p->fork && p->join && p->fin) aux_give(p->device, AuxSet{p->aux, p->fork, p->join, p->fin});
     delete p;
     return 0;
 }
@@ -501,13 +510,17 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
             dftb_plan_destroy(p);
             return fail(DFTB_ECUDA, "stream/event creation failed");
         }
-        p->aux = a.s; p->fork = a.fork; p->join = a.join;
+        p->aux = a.s; p->fork = a.fork; p->join = a.join; p->fin = a.fin;
     }
     TRACE("streams", tr);
     // allocation rounded up to 64 MiB so the pool's blocks are interchangeable between the
     // slightly different batch sizes that follow each other through the pipeline
     const size_t alloc_bytes = (p->mem_bytes + ((size_t)64 << 20) - 1) & ~(((size_t)64 << 20) - 1);
-    cudaError_t ce = cudaMallocAsync((void **)&p->mem, alloc_bytes, st);
+    // allocation and upload on the plan's own aux stream, synchronized here: on the caller's
+    // stream they would queue behind that stream's previous batch, and the synchronization
+    // below would block plan creation until it finished (the labeling pipeline creates the
+    // next batch's plan while the current one runs on the same stream)
+    cudaError_t ce = cudaMallocAsync((void **)&p->mem, alloc_bytes, p->aux);
     TRACE("malloc", tr);
     if (ce != cudaSuccess) {
         p->mem = nullptr;
@@ -518,9 +531,9 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
     std::vector<unsigned char> blob(p->in_bytes, 0);
     for (auto &u : ups)
         if (u.bytes) std::memcpy(blob.data() + u.off, u.src, u.bytes);
-    ce = cudaMemcpyAsync(p->mem, blob.data(), p->in_bytes, cudaMemcpyHostToDevice, st);
+    ce = cudaMemcpyAsync(p->mem, blob.data(), p->in_bytes, cudaMemcpyHostToDevice, p->aux);
     TRACE("copy", tr);
-    if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);  // blob is pageable and local
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(p->aux);  // blob is pageable and local
     TRACE("sync", tr);
     if (ce != cudaSuccess) {
         dftb_plan_destroy(p);
@@ -685,6 +698,8 @@ int dftb_plan_run(dftb_plan *p, void *stream) {
         }
     }
     mark(p, 3, st);
+    CK(cudaEventRecord(p->fin, st));
+    p->fin_rec = true;
     return 0;
 }
 
@@ -754,6 +769,12 @@ int dftb_plan_fetch(dftb_plan *p, dftb_results *r, void *stream) {
     const int nm = d.n_mol, mi = d.max_it;
     std::vector<double> hist((size_t)nm * mi);
     std::vector<int> it(nm);
+    // after dftb_plan_run: copy on the aux stream once this plan's work is done, so the wait
+    // does not include later work the caller already queued on its stream
+    if (p->fin_rec && p->aux) {
+        CK(cudaStreamWaitEvent(p->aux, p->fin, 0));
+        st = p->aux;
+    }
     CK(cudaMemcpyAsync(hist.data(), d.hist, sizeof(double) * hist.size(), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(it.data(), d.iters, sizeof(int) * nm, cudaMemcpyDeviceToHost, st));
     if (r->E_comp) CK(cudaMemcpyAsync(r->E_comp, d.comp, sizeof(double) * 5 * nm, cudaMemcpyDeviceToHost, st));

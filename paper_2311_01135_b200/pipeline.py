@@ -36,7 +36,7 @@ from .batch import check
 from .constants import HARTREE_TO_EV
 from .errors import DeskDFTError
 from .molio import GeometryManifest
-from .scf import SCFOptions, properties, scf_batch
+from .scf import SCFOptions, finish_batch, properties, scf_batch, start_batch
 
 log = logging.getLogger("paper_2311_01135_b200.pipeline")
 
@@ -114,19 +114,39 @@ def label_batches(batches, basis, opts: SCFOptions, workers: int = 3, device: in
         todo.put(None)
 
     def worker():
+        # one batch queued ahead on this worker's stream: the next batch is packed, planned and
+        # enqueued before the current one is waited for, so the host work (packing, plan
+        # creation, result objects) never leaves the GPU without this worker's next batch
         torch.cuda.set_device(dev)
         stream = torch.cuda.Stream(device=dev)
+        pending = None
+
+        def finish(job):
+            k, mols, plan, t0, err = job
+            if err is None:
+                try:
+                    res = finish_batch(plan, opts, errors="return")
+                except Exception as exc:       # a failure of the whole batch: every slot gets it
+                    res = [exc] * len(mols)
+            else:
+                res = [err] * len(mols)
+            done.put((k, res, time.monotonic() - t0))
+
         while True:
             item = todo.get()
             if item is None:
-                return
+                break
             k, mols = item
             t0 = time.monotonic()
             try:
-                res = scf_batch(mols, basis, opts, errors="return", stream=stream.cuda_stream)
-            except Exception as exc:           # a failure of the whole batch: every slot gets it
-                res = [exc] * len(mols)
-            done.put((k, res, time.monotonic() - t0))
+                job = (k, mols, start_batch(mols, basis, opts, stream=stream.cuda_stream), t0, None)
+            except Exception as exc:
+                job = (k, mols, None, t0, exc)
+            if pending is not None:
+                finish(pending)
+            pending = job
+        if pending is not None:
+            finish(pending)
 
     threads = [threading.Thread(target=worker, daemon=True) for _ in range(nthr)]
     for t in threads:

@@ -105,11 +105,29 @@ def scf_batch(mols: list[Molecule], b: BasisSet, opts: SCFOptions | None = None,
     opts = opts or SCFOptions()
     if not mols:
         return []
-    with Plan(list(mols), b, opts.engine(), stream=stream) as plan:
+    return finish_batch(start_batch(mols, b, opts, stream), opts, errors)
+
+
+def start_batch(mols: list[Molecule], b: BasisSet, opts: SCFOptions, stream=None) -> Plan:
+    """First half of scf_batch: pack, create the device plan and enqueue the whole SCF on
+    `stream` without waiting (the labeling pipeline prepares the next batch meanwhile)."""
+    plan = Plan(list(mols), b, opts.engine(), stream=stream)
+    try:
         plan.run()
+    except BaseException:
+        plan.close()
+        raise
+    return plan
+
+
+def finish_batch(plan: Plan, opts: SCFOptions, errors: str = "raise") -> list:
+    """Second half of scf_batch: wait for the plan, copy the results back, release it."""
+    try:
         res = plan.fetch()
+    finally:
+        plan.close()
     out = []
-    for m in range(len(mols)):
+    for m in range(int(plan.pk.n_mol)):
         err = status_error(int(res.status[m]))
         if err is not None:
             if errors == "raise":
