@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -176,6 +177,10 @@ int dftb_plan_destroy(dftb_plan *p) {
     return 0;
 }
 
+#ifndef PLAN_THREADS
+#define PLAN_THREADS 4   // host threads for the per-molecule pair planning
+#endif
+
 // QM1B_TRACE=1: host-time trace of plan creation phases (stderr)
 static double trace_ms() {
     static const bool on = std::getenv("QM1B_TRACE") != nullptr;
@@ -211,13 +216,16 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
         return fail(DFTB_EINVAL, "atom/shell counts do not add up");
     }
     if (p->natom_max > 96) { delete p; return fail(DFTB_ERESOURCE, "more than 96 atoms in a molecule"); }
-    std::vector<int64_t> npairs_cls(3 * nm);
+    std::vector<double> emin(in->n_shell);
+    for (int s = 0; s < in->n_shell; ++s)
+        emin[s] = std::min(in->shell_exp[3 * s], std::min(in->shell_exp[3 * s + 1], in->shell_exp[3 * s + 2]));
     for (int m = 0; m < nm; ++m) {
-        int n = 0;
+        int n = 0, nl = 0;
         const int s0 = shell0[m], ns = in->mol_nshell[m];
         for (int s = s0; s < s0 + ns; ++s) {
             s_ao[s] = n;
             n += in->shell_kind[s] ? 4 : 1;
+            nl += in->shell_kind[s] ? 1 : 0;
             const int la = in->shell_atom[s];
             if (la < 0 || la >= in->mol_natom[m]) { delete p; return fail(DFTB_EINVAL, "shell_atom out of range"); }
             s_atom_g[s] = atom0[m] + la;
@@ -226,56 +234,63 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
         if (in->mol_nocc[m] > n) { delete p; return fail(DFTB_EINVAL, "more occupied orbitals than basis functions"); }
         p->nao[m] = n;
         p->nmax = std::max(p->nmax, n);
-        pair0[m] = (int)p_sa.size();
-        for (int cls = 0; cls < 3; ++cls) {  // 0 LL, 1 LS (L first), 2 SS
-            int cnt = 0;
+        const int nsg = ns - nl;   // class sizes: 0 LL, 1 LS (L first), 2 SS
+        npl[3 * m] = nl * (nl + 1) / 2;
+        npl[3 * m + 1] = nl * nsg;
+        npl[3 * m + 2] = nsg * (nsg + 1) / 2;
+        pair0[m + 1] = pair0[m] + npl[3 * m] + npl[3 * m + 1] + npl[3 * m + 2];
+    }
+    p_sa.resize((size_t)pair0[nm]);
+    p_sb.resize((size_t)pair0[nm]);
+    // class lists of every molecule, each ordered by how slowly the pair's overlap decays:
+    // key mu_min R^2 with mu_min the smallest alpha beta / (alpha + beta) of its primitive
+    // pairs (= that of the two smallest exponents: the expression increases in both), a
+    // geometric stand-in for the Schwarz bound.  The ERI kernels run 32 consecutive kets per
+    // warp; kets of similar extent share their primitive screens and Schwarz outcome.  Ties
+    // by list position, so the order is deterministic.  Molecules are independent: a few
+    // host threads share them (the sorts took 7 ms per 256-molecule batch on one core).
+    auto fill = [&](int m_begin, int m_end) {
+        struct PairKey { double key; int x, y, pos; };
+        std::vector<PairKey> cls_pairs[3];
+        for (int m = m_begin; m < m_end; ++m) {
+            const int s0 = shell0[m], ns = in->mol_nshell[m];
+            for (int c = 0; c < 3; ++c) cls_pairs[c].clear();
             for (int a = s0; a < s0 + ns; ++a)
                 for (int b2 = s0; b2 <= a; ++b2) {
                     const int ka = in->shell_kind[a], kb = in->shell_kind[b2];
                     const int c = (ka && kb) ? 0 : (ka || kb) ? 1 : 2;
-                    if (c != cls) continue;
                     int x = a, y = b2;
-                    if (in->shell_kind[x] < in->shell_kind[y]) std::swap(x, y);
-                    p_sa.push_back(x);
-                    p_sb.push_back(y);
-                    ++cnt;
-                }
-            npl[3 * m + cls] = cnt;
-#ifndef PAIR_SORT
-#define PAIR_SORT 1
-#endif
-            if (PAIR_SORT && cnt > 1) {
-                // order the class list by how slowly the pair's overlap decays: mu_min R^2 with
-                // mu_min the smallest alpha beta / (alpha + beta) of its primitive pairs (a
-                // geometric stand-in for the Schwarz bound), ascending.  The ERI kernels run 32
-                // consecutive kets per warp; kets of similar extent share their primitive screens
-                // and Schwarz outcome.  Stable, so the order is deterministic.
-                const size_t beg = p_sa.size() - (size_t)cnt;
-                std::vector<std::pair<double, int>> key((size_t)cnt);
-                for (int k = 0; k < cnt; ++k) {
-                    const int x = p_sa[beg + k], y = p_sb[beg + k];
+                    if (ka < kb) std::swap(x, y);
                     const double *A = in->atom_xyz + 3 * (size_t)(atom0[m] + in->shell_atom[x]);
                     const double *B = in->atom_xyz + 3 * (size_t)(atom0[m] + in->shell_atom[y]);
                     const double r2 = (A[0] - B[0]) * (A[0] - B[0]) + (A[1] - B[1]) * (A[1] - B[1]) +
                                       (A[2] - B[2]) * (A[2] - B[2]);
-                    double mu = 1e300;
-                    for (int i = 0; i < 3; ++i)
-                        for (int j = 0; j < 3; ++j) {
-                            const double al = in->shell_exp[3 * x + i], be = in->shell_exp[3 * y + j];
-                            mu = std::min(mu, al * be / (al + be));
-                        }
-                    key[k] = {mu * r2, k};
+                    const double al = emin[x], be = emin[y];
+                    cls_pairs[c].push_back({al * be / (al + be) * r2, x, y, (int)cls_pairs[c].size()});
                 }
-                std::stable_sort(key.begin(), key.end(),
-                                 [](const std::pair<double, int> &u, const std::pair<double, int> &v) { return u.first < v.first; });
-                std::vector<int> sa((size_t)cnt), sb((size_t)cnt);
-                for (int k = 0; k < cnt; ++k) { sa[k] = p_sa[beg + key[k].second]; sb[k] = p_sb[beg + key[k].second]; }
-                for (int k = 0; k < cnt; ++k) { p_sa[beg + k] = sa[k]; p_sb[beg + k] = sb[k]; }
+            int o = pair0[m];
+            for (int cls = 0; cls < 3; ++cls) {
+                auto &v = cls_pairs[cls];
+#ifndef PAIR_SORT
+#define PAIR_SORT 1
+#endif
+                if (PAIR_SORT && v.size() > 1)
+                    std::sort(v.begin(), v.end(), [](const PairKey &u, const PairKey &w) {
+                        return u.key < w.key || (u.key == w.key && u.pos < w.pos);
+                    });
+                for (const PairKey &k : v) { p_sa[o] = k.x; p_sb[o] = k.y; ++o; }
             }
         }
+    };
+    {
+        const int nth = std::max(1, std::min(PLAN_THREADS, nm / 16));
+        std::vector<std::thread> th;
+        for (int t = 1; t < nth; ++t) th.emplace_back(fill, (int)((int64_t)nm * t / nth), (int)((int64_t)nm * (t + 1) / nth));
+        fill(0, nm / nth);
+        for (auto &x : th) x.join();
     }
-    pair0[nm] = (int)p_sa.size();
     const int npair = pair0[nm];
+    TRACE("plan:pairs", tr);
     // quartet-class prefixes (6 classes) + Schwarz pair-class prefixes (3)
     std::vector<int64_t> cls0((NCLS + 3) * (size_t)(nm + 1), 0);
     for (int m = 0; m < nm; ++m) {
@@ -353,6 +368,7 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
         V0[m + 1] = V0[m] + (int64_t)ncx * N * N;
     }
     p->grid0[nm] = a_grid0[in->n_atom];
+    TRACE("plan:ctas", tr);
     // XC CTAs grouped by AO-count bucket (NQ = 4 * ceil(N / 16))
     std::vector<int> xc_sorted;
     for (int bkt = 0; bkt < 6; ++bkt) {
@@ -377,21 +393,20 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
     std::stable_sort(mol_order.begin(), mol_order.end(), [&](int a, int c) { return p->nao[a] > p->nao[c]; });
     // J/K CTAs: largest work first within each bucket
     {
-        auto work = [&](int c) {
-            int64_t w = 0;
+        std::vector<int64_t> work(jk_mol.size(), 0);
+        for (size_t c = 0; c < jk_mol.size(); ++c)
             for (int i = jk_i0[c]; i < jk_i1[c]; ++i) {
                 const int64_t A = i / 4 + 1;
-                w += (int64_t)(i + 1) * (A * (A + 1) / 2);
+                work[c] += (int64_t)(i + 1) * (A * (A + 1) / 2);
             }
-            return w;
-        };
         int off = 0;
         for (int bkt = 0; bkt < 6; ++bkt) {
             std::stable_sort(jk_sorted.begin() + off, jk_sorted.begin() + off + p->jk_bucket_n[bkt],
-                             [&](int a, int c) { return work(a) > work(c); });
+                             [&](int a, int c) { return work[a] > work[c]; });
             off += p->jk_bucket_n[bkt];
         }
     }
+    TRACE("plan:sort", tr);
     const int64_t npts_tot = a_grid0[in->n_atom];
     const int njk = (int)jk_mol.size(), nxc = (int)xc_mol.size();
     const int64_t mat = p->mat0[nm];
