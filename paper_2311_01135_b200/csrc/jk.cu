@@ -36,8 +36,10 @@ namespace dftb {
 #ifndef JK_NBUF_MAX
 #define JK_NBUF_MAX 2                          // staging buffers per CTA
 #endif
-constexpr int JK_WARPS = 4;                    // one store row per warp
-constexpr int JK_THREADS = 32 * JK_WARPS;
+// warps per CTA (one store row per warp): 4 for the buckets up to 64 AOs (3 CTAs per SM),
+// 8 for the larger ones (measured on B200: NB = 80 f32 331 -> 221 us per launch, NB = 64
+// 1.55 -> 1.59 ms)
+template <int NB> constexpr int jk_warps() { return NB > 64 ? 8 : 4; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
@@ -92,8 +94,9 @@ __device__ __forceinline__ double shfl_x(double v, int o) { return __shfl_xor_sy
 // Shared-memory plan of one bucket: NBUF staging buffers of CR rows, padded rho, G_i
 // reduction scratch.  Double buffering (then rows per chunk) is reduced for the largest
 // buckets to fit 227 KB.
-template <typename ST, int NB>
+template <typename ST, int NB, int JK_WARPS = jk_warps<NB>()>
 struct JKPlan {
+    static constexpr int JK_THREADS = 32 * JK_WARPS;
     static constexpr int AMAX = NB / 4;
     static constexpr int LMAX = 8 * AMAX * (AMAX + 1);
     static constexpr size_t row_bytes = (size_t)LMAX * sizeof(ST);
@@ -107,7 +110,9 @@ struct JKPlan {
         JK_NBUF_MAX > 1 && fixed + 2 * JK_WARPS * row_bytes <= cap &&
                 !(ctas(fixed + JK_WARPS * row_bytes) > ctas(fixed + 2 * JK_WARPS * row_bytes))
             ? 2 : 1;
-    static constexpr int CR = fixed + NBUF * JK_WARPS * row_bytes <= cap ? JK_WARPS : JK_WARPS / 2;
+    static constexpr int CR = fixed + NBUF * JK_WARPS * row_bytes <= cap       ? JK_WARPS
+                              : fixed + NBUF * (JK_WARPS / 2) * row_bytes <= cap ? JK_WARPS / 2
+                                                                                 : JK_WARPS / 4;
     static constexpr size_t bytes = fixed + NBUF * CR * row_bytes;
     static_assert(bytes <= 227 * 1024, "J/K bucket does not fit in shared memory");
 };
@@ -134,8 +139,9 @@ __device__ __forceinline__ int tri32(int a) { return (a * (a + 1)) >> 1; }
 // NB: AO-count bound of the bucket (multiple of 16) — fixes the padded rho stride, the
 // staging size and the number of J_Q units each thread owns.
 template <typename ST, int NB>
-__global__ void __launch_bounds__(JK_THREADS) k_jk(DevBatch b, const int *ctas) {
+__global__ void __launch_bounds__(32 * jk_warps<NB>(), NB > 64 ? 2 : NB > 32 ? 3 : 4) k_jk(DevBatch b, const int *ctas) {
     using PL = JKPlan<ST, NB>;
+    constexpr int JK_THREADS = PL::JK_THREADS;
     constexpr int VW = 16 / (int)sizeof(ST);                   // elements per 16-byte unit
     constexpr int LMAX = PL::LMAX, NBUF = PL::NBUF, CR = PL::CR;
     constexpr int KU = (LMAX / VW + JK_THREADS - 1) / JK_THREADS;
@@ -365,7 +371,7 @@ template <typename ST, int NB>
 static void launch_bucket(const DevBatch &b, const int *ctas, int n, cudaStream_t s) {
     const size_t sm = JKPlan<ST, NB>::bytes;
     smem_optin((const void *)k_jk<ST, NB>);
-    k_jk<ST, NB><<<n, JK_THREADS, sm, s>>>(b, ctas);
+    k_jk<ST, NB><<<n, JKPlan<ST, NB>::JK_THREADS, sm, s>>>(b, ctas);
 }
 
 template <typename ST>
