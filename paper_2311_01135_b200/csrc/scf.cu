@@ -525,39 +525,62 @@ __device__ void diis_extrapolate(const DevBatch &b, int m, int N, const double *
         ar.B[t] = (r == c) ? 1.0 : 0.0;
     }
     __syncthreads();
-    if (tid < 32) warp_jacobi_eigs(ar.A, n1, ar);
-    const double *Ad = ar.A;
-    if (tid == 0) {
-        double mx = 0.0, mn = 1e308;
-        for (int i = 0; i < n1; ++i) {
-            const double e = fabs(Ad[i * n1 + i]);
-            mx = fmax(mx, e);
-            mn = fmin(mn, e);
-        }
-        const bool fallback = !(mn > 0.0) || (mx / mn > 1e12);
-        ar.scal[1] = fallback ? 1.0 : 0.0;
-        if (!fallback) {  // Gaussian elimination with partial pivoting on the bordered system
-            double Mx[10][11];
-            for (int r = 0; r < n1; ++r) {
-                for (int c = 0; c < n1; ++c) Mx[r][c] = ar.Bs[r * n1 + c];
-                Mx[r][n1] = (r == nh) ? 1.0 : 0.0;
+    if (tid < 32) {
+        const int lane = tid;
+        warp_jacobi_eigs(ar.A, n1, ar);
+        __syncwarp();
+        bool fallback = false;
+        if (lane == 0) {
+            const double *Ad = ar.A;
+            double mx = 0.0, mn = 1e308;
+            for (int i = 0; i < n1; ++i) {
+                const double e = fabs(Ad[i * n1 + i]);
+                mx = fmax(mx, e);
+                mn = fmin(mn, e);
             }
+            fallback = !(mn > 0.0) || (mx / mn > 1e12);
+            ar.scal[1] = fallback ? 1.0 : 0.0;
+        }
+        fallback = __shfl_sync(0xffffffffu, fallback, 0);
+        if (!fallback) {
+            // Gaussian elimination with partial pivoting on the bordered system, by the warp in
+            // shared memory (the same operations in the same order per element as a serial
+            // elimination; a thread-local 10 x 11 array cost a local-memory round trip per
+            // element update): Mx in ar.A (row stride W), row multipliers in ar.sn
+            double *Mx = ar.A, *fr = ar.sn;
+            const int W = n1 + 1;
+            __syncwarp();
+            for (int t = lane; t < n1 * W; t += 32) {
+                const int r = t / W, k = t - r * W;
+                Mx[t] = k < n1 ? ar.Bs[r * n1 + k] : (r == nh ? 1.0 : 0.0);
+            }
+            __syncwarp();
             for (int c = 0; c < n1; ++c) {
                 int piv = c;
                 for (int r = c + 1; r < n1; ++r)
-                    if (fabs(Mx[r][c]) > fabs(Mx[piv][c])) piv = r;
-                if (piv != c)
-                    for (int k = 0; k <= n1; ++k) { double t = Mx[c][k]; Mx[c][k] = Mx[piv][k]; Mx[piv][k] = t; }
-                for (int r = c + 1; r < n1; ++r) {
-                    const double f = Mx[r][c] / Mx[c][c];
-                    for (int k = c; k <= n1; ++k) Mx[r][k] -= f * Mx[c][k];
+                    if (fabs(Mx[r * W + c]) > fabs(Mx[piv * W + c])) piv = r;
+                __syncwarp();
+                if (piv != c && lane <= n1) {
+                    const double t = Mx[c * W + lane];
+                    Mx[c * W + lane] = Mx[piv * W + lane];
+                    Mx[piv * W + lane] = t;
                 }
+                __syncwarp();
+                for (int r = c + 1 + lane; r < n1; r += 32) fr[r] = Mx[r * W + c] / Mx[c * W + c];
+                __syncwarp();
+                const int wk = n1 + 1 - c;
+                for (int t = lane; t < (n1 - c - 1) * wk; t += 32) {
+                    const int r = c + 1 + t / wk, k = c + t % wk;
+                    Mx[r * W + k] -= fr[r] * Mx[c * W + k];
+                }
+                __syncwarp();
             }
-            for (int r = n1 - 1; r >= 0; --r) {
-                double s = Mx[r][n1];
-                for (int k = r + 1; k < n1; ++k) s -= Mx[r][k] * ar.cf[k];
-                ar.cf[r] = s / Mx[r][r];
-            }
+            if (lane == 0)
+                for (int r = n1 - 1; r >= 0; --r) {
+                    double s = Mx[r * W + n1];
+                    for (int k = r + 1; k < n1; ++k) s -= Mx[r * W + k] * ar.cf[k];
+                    ar.cf[r] = s / Mx[r * W + r];
+                }
         }
     }
     __syncthreads();
