@@ -358,7 +358,9 @@ def run_ours(args, ws, rank, local):
     # F batches in flight (paper_2311_01135_b200.pipeline.label_batches)
     from paper_2311_01135_b200.pipeline import label_batches
 
-    list(label_batches(batches, b, opts, workers=F))      # warm (plan pool, threads)
+    # warm-up (untimed): enough batches that every worker reaches its steady state of one
+    # batch queued ahead (2F plans alive), so the memory pool is grown before timing
+    list(label_batches([batches[k % F] for k in range(max(args.warmup, 2 * F))], b, opts, workers=F))
     barrier()
     torch.cuda.synchronize()
     t = time.perf_counter()
