@@ -112,10 +112,12 @@ int dftb_scf_batch(const dftb_batch_in *in, const dftb_opts *opts, dftb_results 
 
 /* Plan lifecycle (device-resident inputs; used by the benchmark's `value` arm). */
 int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *stream, dftb_plan **plan);
-int dftb_plan_destroy(dftb_plan *plan);
+int dftb_plan_destroy(dftb_plan *plan);   /* frees after the plan's queued work, stream-ordered */
 int dftb_plan_run(dftb_plan *plan, void *stream);              /* setup + SCF loop */
 int dftb_plan_begin(dftb_plan *plan, void *stream);            /* setup + core guess only */
 int dftb_plan_iterate(dftb_plan *plan, int32_t it, void *stream); /* one SCF iteration */
+/* Blocks until this plan's last dftb_plan_run has completed (not any later work queued on
+ * `stream` by other plans) and copies the results to host memory on the plan's own stream. */
 int dftb_plan_fetch(dftb_plan *plan, dftb_results *out, void *stream);
 int dftb_plan_info(const dftb_plan *plan, int64_t *info, int n_info);  /* sizes, see plan.cu */
 
