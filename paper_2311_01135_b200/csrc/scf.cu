@@ -420,7 +420,9 @@ __device__ __forceinline__ double seq_sum(int n, F load) {
 }
 
 // J from owner + scattered partials, K = -(G + G^T)/4 from G rows (fixed-order sums).
-__device__ void reduce_jk(const DevBatch &b, int m, int N, double *J, double *K) {
+// (and V_xc = W + W^T with W the fixed-order sum of the per-XC-CTA partials)
+template <bool WITH_V>
+__device__ void reduce_jkv(const DevBatch &b, int m, int N, double *J, double *K, double *Vx) {
     const int tid = threadIdx.x;
     const int64_t npp = tri(N);
     const double *Jp = b.Jpart + b.m_Jp0[m];
@@ -436,7 +438,17 @@ __device__ void reduce_jk(const DevBatch &b, int m, int N, double *J, double *K)
     }
     const double *Gp = b.Gpart + b.m_G0[m];   // [ncj][N][N] per-CTA exchange partials
     const int64_t NN = (int64_t)N * N;
-    for (int t = tid; t < N * N; t += SCF_THREADS) K[t] = seq_sum(ncj, [&](int c) { return Gp[c * NN + t]; });
+    // the exchange and V_xc partial sums in one loop: both load streams in flight together
+    const double *Vp = b.Vpart + b.m_V0[m];
+    const int ncx = WITH_V ? b.m_xccta0[m + 1] - b.m_xccta0[m] : 0;
+    for (int t = tid; t < N * N; t += SCF_THREADS) {
+        const double kv = seq_sum(ncj, [&](int c) { return Gp[c * NN + t]; });
+        if constexpr (WITH_V) {
+            const double vv = seq_sum(ncx, [&](int c) { return Vp[(int64_t)c * NN + t]; });
+            Vx[t] = vv;
+        }
+        K[t] = kv;
+    }
     __syncthreads();
     for (int t = tid; t < N * N; t += SCF_THREADS) {
         const int a = t / N, c = t % N;
@@ -446,6 +458,15 @@ __device__ void reduce_jk(const DevBatch &b, int m, int N, double *J, double *K)
             K[c * N + a] = g;
         } else if (a == c) {
             K[t] = -0.5 * K[t];
+        }
+        if constexpr (WITH_V) {
+            if (a < c) {
+                const double v = Vx[a * N + c] + Vx[c * N + a];
+                Vx[a * N + c] = v;
+                Vx[c * N + a] = v;
+            } else if (a == c) {
+                Vx[t] = 2.0 * Vx[t];
+            }
         }
     }
 }
@@ -482,7 +503,7 @@ __device__ double reduce_exc(const DevBatch &b, int m) {
 __global__ void __launch_bounds__(SCF_THREADS) k_reduce(DevBatch b, int which) {
     const int m = blockIdx.x, N = b.m_nao[m];
     const int64_t o = b.m_mat0[m];
-    if (which == 1) reduce_jk(b, m, N, b.J + o, b.K + o);
+    if (which == 1) reduce_jkv<false>(b, m, N, b.J + o, b.K + o, nullptr);
     else {
         reduce_vxc(b, m, N, b.Vxc + o);
         if (threadIdx.x == 0) b.comp[5 * m + 4] = reduce_exc(b, m);
@@ -629,8 +650,7 @@ __global__ void __launch_bounds__(SCF_THREADS, 2) k_post(DevBatch b, PostArgs pa
     long long *dbg = b.dbg ? b.dbg + 16 * m : nullptr;
     auto tick = [&](int k) { if (dbg && tid == 0) { long long t = clock64(); dbg[k] += t - tl; tl = t; } };
     if (it >= 0) {
-        reduce_jk(b, m, N, J, K);
-        reduce_vxc(b, m, N, Vx);
+        reduce_jkv<true>(b, m, N, J, K, Vx);
         __syncthreads();
         tick(0);
         // (4) F and (5) energies
