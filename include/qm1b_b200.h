@@ -51,6 +51,7 @@ enum {
 #define DFTB_ST_NEG_WEIGHT       2
 #define DFTB_ST_XC_NONFINITE     4
 #define DFTB_ST_NO_ORBITALS      8
+#define DFTB_ST_SINGULAR        16   /* no overlap eigenvalue above the 1e-7 linear-dependence cut */
 
 typedef struct dftb_plan dftb_plan;
 

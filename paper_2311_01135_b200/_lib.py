@@ -16,8 +16,17 @@ from .errors import DeskDFTError, DeviceError, DimensionError, ResourceLimitErro
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libqm1b_b200.so")
-# development override (A/B timing of two builds in one process tree); never set in production
-LIB_PATH = os.environ.get("QM1B_B200_LIB", LIB_PATH)
+# Development override for same-box A/B timing of two builds (tools/); it must name a file
+# inside this repository and is reported on stderr, so it cannot silently swap the product.
+_DEV_LIB = os.environ.get("QM1B_B200_DEV_LIB")
+if _DEV_LIB:
+    _repo = os.path.dirname(_HERE)
+    if not os.path.realpath(_DEV_LIB).startswith(os.path.realpath(_repo) + os.sep):
+        raise RuntimeError(f"QM1B_B200_DEV_LIB={_DEV_LIB} is outside the repository")
+    import sys as _sys
+
+    print(f"[qm1b_b200] development library override: {_DEV_LIB}", file=_sys.stderr)
+    LIB_PATH = _DEV_LIB
 NMAX = 96
 
 c_i32p = ctypes.POINTER(ctypes.c_int32)
@@ -53,7 +62,7 @@ class Results(ctypes.Structure):
     ]
 
 
-ST_OVERLAP_NOT_PD, ST_NEG_WEIGHT, ST_XC_NONFINITE, ST_NO_ORBITALS = 1, 2, 4, 8
+ST_OVERLAP_NOT_PD, ST_NEG_WEIGHT, ST_XC_NONFINITE, ST_NO_ORBITALS, ST_SINGULAR = 1, 2, 4, 8, 16
 
 _lib = None
 

@@ -8,6 +8,7 @@ templates) is computed once per (element, grid level) and reused.
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -44,29 +45,40 @@ class PackedBatch:
 
 
 class _TemplateCache:
-    """Concatenated atom-centred grid templates for the (Z, level) keys seen so far."""
+    """Concatenated atom-centred grid templates for the (Z, level) keys seen so far.
+
+    Shared by the labeling pipeline's worker threads (one plan per thread): a key's
+    (offset, count) and the chunk it points to are published together under the lock, and
+    array() returns a snapshot that contains every template whose key a caller already got
+    (templates are only ever appended)."""
 
     def __init__(self):
         self.index: dict[tuple[int, int], tuple[int, int]] = {}
         self.chunks: list[np.ndarray] = []
         self.total = 0
         self._cat: np.ndarray | None = None
+        self._lock = threading.Lock()
 
     def get(self, z: int, level: int) -> tuple[int, int]:
         key = (z, level)
-        if key not in self.index:
-            t = atom_template(z, level)
-            self.index[key] = (self.total, len(t))
-            self.chunks.append(t)
-            self.total += len(t)
-            self._cat = None
-        return self.index[key]
+        hit = self.index.get(key)
+        if hit is not None:
+            return hit
+        t = atom_template(z, level)          # outside the lock: pure function of (z, level)
+        with self._lock:
+            if key not in self.index:
+                self.chunks.append(t)
+                self.index[key] = (self.total, len(t))
+                self.total += len(t)
+                self._cat = None
+            return self.index[key]
 
     def array(self) -> np.ndarray:
-        if self._cat is None:
-            self._cat = (np.ascontiguousarray(np.concatenate(self.chunks))
-                         if self.chunks else np.zeros((0, 4)))
-        return self._cat
+        with self._lock:
+            if self._cat is None:
+                self._cat = (np.ascontiguousarray(np.concatenate(self.chunks))
+                             if self.chunks else np.zeros((0, 4)))
+            return self._cat
 
 
 _TEMPLATES = _TemplateCache()

@@ -85,8 +85,25 @@ struct dftb_plan {
     cudaStream_t aux = nullptr;     // J/K runs here, concurrently with XC on the caller's stream
     cudaEvent_t fork = nullptr, join = nullptr;
     cudaEvent_t fin = nullptr;      // this plan's last work on the caller's stream (fetch / free wait on it)
-    bool fin_rec = false;
+    bool fin_rec = false;           // fin holds the end of the last completed enqueueing call
+    bool dirty = false;             // an enqueueing call started after fin was last recorded
+    cudaStream_t last = nullptr;    // stream of the last enqueueing call
 };
+
+// Every entry point that enqueues device work brackets it with enq_begin / enq_end: fin then
+// marks the end of this plan's submitted work on the stream the caller used, so fetch and
+// the stream-ordered free wait for exactly this plan's work (not later batches the caller has
+// queued on the same stream), and a call that failed partway is still covered (dirty).
+static void enq_begin(dftb_plan *p, cudaStream_t st) {
+    p->dirty = true;
+    p->last = st;
+}
+static void enq_end(dftb_plan *p, cudaStream_t st) {
+    if (p->fin && cudaEventRecord(p->fin, st) == cudaSuccess) {
+        p->fin_rec = true;
+        p->dirty = false;
+    }
+}
 
 // ------------------------------------------------------------------ Boys table (per device)
 static double *g_boys[64] = {nullptr};
@@ -165,7 +182,9 @@ int dftb_plan_destroy(dftb_plan *p) {
     // the free is ordered after this plan's last submitted work (fin) on the aux stream, not
     // after whatever the caller's stream holds by now (the pipeline queues the next batch there)
     if (p->aux && p->fin) {
-        if (!p->fin_rec && p->stream) cudaEventRecord(p->fin, p->stream);   // no run: all of st so far
+        // nothing recorded yet, or a call that failed partway: everything on its stream so far
+        // (NULL = the legacy stream is a valid record target)
+        if (!p->fin_rec || p->dirty) cudaEventRecord(p->fin, p->dirty ? p->last : p->stream);
         cudaStreamWaitEvent(p->aux, p->fin, 0);
     }
     if (p->mem) cudaFreeAsync(p->mem, p->aux ? p->aux : p->stream);   // back to the retained pool
@@ -216,6 +235,18 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
         return fail(DFTB_EINVAL, "atom/shell counts do not add up");
     }
     if (p->natom_max > 96) { delete p; return fail(DFTB_ERESOURCE, "more than 96 atoms in a molecule"); }
+    if (in->n_tmpl < 0 || (in->n_tmpl > 0 && (!in->tmpl_xyzw || !in->atom_tmpl0 || !in->atom_tmpln))) {
+        delete p;
+        return fail(DFTB_EINVAL, "grid templates: bad count or null arrays");
+    }
+    if (in->n_tmpl > 0)
+        for (int a = 0; a < in->n_atom; ++a) {
+            const int64_t t0 = in->atom_tmpl0[a], tn = in->atom_tmpln[a];
+            if (t0 < 0 || tn < 0 || t0 + tn > in->n_tmpl) {   // k_grid reads tmpl[t0 .. t0 + tn)
+                delete p;
+                return fail(DFTB_EINVAL, "atom grid template range outside [0, n_tmpl)");
+            }
+        }
     std::vector<double> emin(in->n_shell);
     for (int s = 0; s < in->n_shell; ++s)
         emin[s] = std::min(in->shell_exp[3 * s], std::min(in->shell_exp[3 * s + 1], in->shell_exp[3 * s + 2]));
@@ -651,8 +682,10 @@ static cudaError_t join(dftb_plan *p, cudaStream_t st) {
 int dftb_plan_begin(dftb_plan *p, void *stream) {
     if (!p) return fail(DFTB_EINVAL, "null plan");
     cudaStream_t st = (cudaStream_t)stream;
+    enq_begin(p, st);
     const DevBatch &d = p->d;
     p->launches = 0;
+    enq_begin(p, st);
     int rc = zero_work(p, st);
     if (rc) return rc;
     mark(p, 0, st);
@@ -673,6 +706,8 @@ int dftb_plan_begin(dftb_plan *p, void *stream) {
     CK(join(p, st));
     CK(cudaGetLastError());
     mark(p, 2, st);
+    enq_end(p, st);
+    enq_end(p, st);
     return 0;
 }
 
@@ -681,6 +716,7 @@ int dftb_plan_iterate(dftb_plan *p, int32_t it, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     const DevBatch &d = p->d;
     const dftb_opts &o = p->opts;
+    enq_begin(p, st);
     // J/K (aux stream) and XC (caller's stream) both read rho and write separate partials:
     // fork/join so their CTAs share the SMs (FP64/XU-heavy vs FP32-heavy, smem fits both)
     CK(fork(p, st));
@@ -690,6 +726,7 @@ int dftb_plan_iterate(dftb_plan *p, int32_t it, void *stream) {
     launch_post(d, p->nmax, it, o.diis_start, o.diis_history, o.damping_factor, o.convergence_std, st);
     p->launches += 1 + njl + nxl;
     CK(cudaGetLastError());
+    enq_end(p, st);
     return 0;
 }
 
@@ -713,8 +750,7 @@ int dftb_plan_run(dftb_plan *p, void *stream) {
         }
     }
     mark(p, 3, st);
-    CK(cudaEventRecord(p->fin, st));
-    p->fin_rec = true;
+    enq_end(p, st);
     return 0;
 }
 
@@ -724,6 +760,7 @@ int dftb_plan_eri_load(dftb_plan *p, int32_t mol, int64_t count, const uint16_t 
                        const uint16_t *k, const uint16_t *l, const double *v, void *stream) {
     if (!p || mol < 0 || mol >= p->d.n_mol) return fail(DFTB_EINVAL, "bad arguments");
     cudaStream_t st = (cudaStream_t)stream;
+    enq_begin(p, st);
     const int64_t npp = p->npp0[mol + 1] - p->npp0[mol];
     const int esz = p->d.eri64 ? 8 : 4;
     const int N = p->nao[mol];
@@ -738,15 +775,18 @@ int dftb_plan_eri_load(dftb_plan *p, int32_t mol, int64_t count, const uint16_t 
     }
     CK(cudaMemcpyAsync(p->mem + p->eri_off + (size_t)e0 * esz, host.data(), host.size(), cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
+    enq_end(p, st);
     return 0;
 }
 
 int dftb_plan_load_grid(dftb_plan *p, const double *pts, const double *w, int64_t n, void *stream) {
     if (!p || n != p->d.n_pts) return fail(DFTB_EINVAL, "grid size does not match the plan");
     cudaStream_t st = (cudaStream_t)stream;
+    enq_begin(p, st);
     CK(cudaMemcpyAsync(p->d.g_xyz, pts, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(p->d.g_w, w, sizeof(double) * n, cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
+    enq_end(p, st);
     return 0;
 }
 
@@ -820,6 +860,7 @@ int dftb_scf_batch(const dftb_batch_in *in, const dftb_opts *opts, dftb_results 
 int dftb_plan_one_electron(dftb_plan *p, void *stream) {
     if (!p) return fail(DFTB_EINVAL, "null plan");
     cudaStream_t st = (cudaStream_t)stream;
+    enq_begin(p, st);
     int rc = zero_work(p, st);
     if (rc) return rc;
     launch_pairs(p->d, st);
@@ -827,26 +868,31 @@ int dftb_plan_one_electron(dftb_plan *p, void *stream) {
     launch_enn(p->d, st);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
+    enq_end(p, st);
     return 0;
 }
 
 int dftb_plan_eri(dftb_plan *p, int screened, void *stream) {
     if (!p) return fail(DFTB_EINVAL, "null plan");
     cudaStream_t st = (cudaStream_t)stream;
+    enq_begin(p, st);
     int rc = zero_work(p, st);
     if (rc) return rc;
     rc = setup_stage(p, st, screened != 0);
     if (rc) return rc;
     CK(cudaStreamSynchronize(st));
+    enq_end(p, st);
     return 0;
 }
 
 int dftb_plan_grid(dftb_plan *p, void *stream) {
     if (!p) return fail(DFTB_EINVAL, "null plan");
     cudaStream_t st = (cudaStream_t)stream;
+    enq_begin(p, st);
     launch_grid(p->d, p->natom_max, st);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
+    enq_end(p, st);
     return 0;
 }
 
@@ -859,6 +905,7 @@ static int upload_rho(dftb_plan *p, const double *rho_host, cudaStream_t st) {
 int dftb_plan_jk(dftb_plan *p, const double *rho_host, double *J_host, double *K_host, void *stream) {
     if (!p) return fail(DFTB_EINVAL, "null plan");
     cudaStream_t st = (cudaStream_t)stream;
+    enq_begin(p, st);
     int rc = upload_rho(p, rho_host, st);
     if (rc) return rc;
     launch_jk(p->d, p->jk_bucket_ctas, p->jk_bucket_n, st);
@@ -868,6 +915,7 @@ int dftb_plan_jk(dftb_plan *p, const double *rho_host, double *J_host, double *K
     if (J_host) CK(cudaMemcpyAsync(J_host, p->d.J, nb, cudaMemcpyDeviceToHost, st));
     if (K_host) CK(cudaMemcpyAsync(K_host, p->d.K, nb, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    enq_end(p, st);
     return 0;
 }
 
@@ -875,6 +923,7 @@ int dftb_plan_jk(dftb_plan *p, const double *rho_host, double *J_host, double *K
 int dftb_plan_xc(dftb_plan *p, const double *rho_host, double *Vxc_host, double *Exc_host, void *stream) {
     if (!p) return fail(DFTB_EINVAL, "null plan");
     cudaStream_t st = (cudaStream_t)stream;
+    enq_begin(p, st);
     int rc = upload_rho(p, rho_host, st);
     if (rc) return rc;
     launch_xc(p->d, p->xc_bucket_ctas, p->xc_bucket_n, p->nsh_max, st);
@@ -894,12 +943,14 @@ int dftb_plan_xc(dftb_plan *p, const double *rho_host, double *Vxc_host, double 
     CK(cudaStreamSynchronize(st));
     for (int s : status) bad |= s & DFTB_ST_XC_NONFINITE;
     if (bad) return fail(DFTB_ENUMERIC, "non-finite functional output (density underflow mishandled)");
+    enq_end(p, st);
     return 0;
 }
 
 int dftb_plan_eval_ao(dftb_plan *p, int32_t mol, double *phi_host, double *grad_host, void *stream) {
     if (!p || mol < 0 || mol >= p->d.n_mol) return fail(DFTB_EINVAL, "bad molecule index");
     cudaStream_t st = (cudaStream_t)stream;
+    enq_begin(p, st);
     const int64_t npts = p->grid0[mol + 1] - p->grid0[mol];
     const int N = p->nao[mol];
     double *buf = nullptr;
@@ -911,6 +962,7 @@ int dftb_plan_eval_ao(dftb_plan *p, int32_t mol, double *phi_host, double *grad_
         CK(cudaMemcpyAsync(grad_host, buf + npts * N, sizeof(double) * 3 * npts * N, cudaMemcpyDeviceToHost, st));
     CK(cudaFreeAsync(buf, st));
     CK(cudaStreamSynchronize(st));
+    enq_end(p, st);
     return 0;
 }
 
@@ -918,6 +970,7 @@ int dftb_plan_roothaan(dftb_plan *p, const double *F_host, double *C_host, doubl
                        void *stream) {
     if (!p) return fail(DFTB_EINVAL, "null plan");
     cudaStream_t st = (cudaStream_t)stream;
+    enq_begin(p, st);
     // S must be present (dftb_plan_one_electron or dftb_plan_set "S"); X from S
     CK(cudaMemsetAsync(p->d.status, 0, sizeof(int) * p->d.n_mol, st));
     launch_orth(p->d, p->nmax, st);
@@ -928,6 +981,7 @@ int dftb_plan_roothaan(dftb_plan *p, const double *F_host, double *C_host, doubl
     if (eps_host) CK(cudaMemcpyAsync(eps_host, p->d.eps, sizeof(double) * NMAX * p->d.n_mol, cudaMemcpyDeviceToHost, st));
     if (nmo_host) CK(cudaMemcpyAsync(nmo_host, p->d.nmo, sizeof(int) * p->d.n_mol, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    enq_end(p, st);
     return 0;
 }
 
@@ -935,6 +989,7 @@ int dftb_plan_eri_compact(dftb_plan *p, int32_t mol, double eps, const double *q
                           uint16_t *oi, uint16_t *oj, uint16_t *ok, uint16_t *ol, double *ov, void *stream) {
     if (!p || mol < 0 || mol >= p->d.n_mol || !count) return fail(DFTB_EINVAL, "bad arguments");
     cudaStream_t st = (cudaStream_t)stream;
+    enq_begin(p, st);
     const int N = p->nao[mol];
     const int64_t npp = (int64_t)N * (N + 1) / 2;
     double *qsp = nullptr;
@@ -968,6 +1023,7 @@ int dftb_plan_eri_compact(dftb_plan *p, int32_t mol, double eps, const double *q
     CK(cudaFreeAsync(qsp, st));
     CK(cudaFreeAsync(rc_, st));
     CK(cudaStreamSynchronize(st));
+    enq_end(p, st);
     return 0;
 }
 
@@ -1082,6 +1138,7 @@ int dftb_diis(const double *F, const double *E, int32_t m, int32_t n, double *ou
 int dftb_plan_kernel_times(dftb_plan *p, int32_t reps, double *ms_jk, double *ms_xc, void *stream) {
     if (!p || reps < 1 || !ms_jk) return fail(DFTB_EINVAL, "bad arguments");
     cudaStream_t st = (cudaStream_t)stream;
+    enq_begin(p, st);
     const DevBatch &d = p->d;
     // the kernels skip molecules whose SCF has finished: clear the flags for the timing
     // and restore them afterwards
@@ -1110,6 +1167,7 @@ int dftb_plan_kernel_times(dftb_plan *p, int32_t reps, double *ms_jk, double *ms
     CK(cudaMemcpyAsync(d.done, done.data(), sizeof(int) * d.n_mol, cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
     CK(cudaGetLastError());
+    enq_end(p, st);
     return 0;
 }
 

@@ -378,8 +378,10 @@ __global__ void __launch_bounds__(SCF_THREADS, 2) k_orth(DevBatch b, int nm) {
             M += ar.dv[i] > 1e-7;
             smax = fmax(smax, ar.dv[i]);
         }
-        if (smax <= 0.0 || M == 0) b.status[m] |= DFTB_ST_OVERLAP_NOT_PD;
-        if (M < b.m_nocc[m] + 0) b.status[m] |= (M < b.m_nocc[m]) ? DFTB_ST_NO_ORBITALS : 0;
+        // scf.py:89-93: not PD if the largest eigenvalue is <= 0, singular if nothing survives
+        if (smax <= 0.0) b.status[m] |= DFTB_ST_OVERLAP_NOT_PD;
+        else if (M == 0) b.status[m] |= DFTB_ST_SINGULAR;
+        if (M < b.m_nocc[m]) b.status[m] |= DFTB_ST_NO_ORBITALS;
         b.nmo[m] = M;
         ar.scal[0] = M;
     }
@@ -636,7 +638,7 @@ __global__ void __launch_bounds__(SCF_THREADS, 2) k_post(DevBatch b, PostArgs pa
     if (b.dbg) ar.dbgp = b.dbg + 16 * m + 14;   // dbg[14], dbg[15]: Jacobi angle / apply cycles
 #endif
     const int N = b.m_nao[m], M = b.nmo[m], nocc = b.m_nocc[m];
-    if (b.status[m] & (DFTB_ST_OVERLAP_NOT_PD | DFTB_ST_NO_ORBITALS)) {
+    if (b.status[m] & (DFTB_ST_OVERLAP_NOT_PD | DFTB_ST_SINGULAR | DFTB_ST_NO_ORBITALS)) {
         if (tid == 0) b.done[m] = 1;
         return;
     }

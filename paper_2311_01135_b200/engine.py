@@ -206,6 +206,8 @@ def status_error(code: int) -> DeskDFTError | None:
     """Map a per-molecule status word to the reference's exception (None if clean)."""
     if code & _lib.ST_OVERLAP_NOT_PD:
         return DeskDFTError("overlap matrix not positive definite")
+    if code & _lib.ST_SINGULAR:
+        return DeskDFTError("overlap matrix singular after linear-dependence drop")
     if code & _lib.ST_NO_ORBITALS:
         return DimensionError("n_occ exceeds the orbital count (basis too small)")
     if code & _lib.ST_NEG_WEIGHT:

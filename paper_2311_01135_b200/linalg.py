@@ -53,12 +53,10 @@ def roothaan_device(F: np.ndarray, S: np.ndarray, n_occ: int = 0):
         import ctypes
         _lib.check(lib.dftb_plan_roothaan(p.h, _lib.ptr(F64), _lib.ptr(C), _lib.ptr(eps),
                                           _lib.ptr(nmo, ctypes.c_int32), p.stream))
-        st = np.zeros(1)
+        status = int(p.fetch(want_C=False).status[0])
     m = int(nmo[0])
-    if m == 0:
-        raise DeskDFTError("overlap matrix singular after linear-dependence drop")
-    s_max = np.linalg.eigvalsh(S64)[-1] if n <= 4 else None
-    if s_max is not None and s_max <= 0:
+    if status & _lib.ST_OVERLAP_NOT_PD:
         raise DeskDFTError("overlap matrix not positive definite")
-    del st
+    if m == 0 or status & _lib.ST_SINGULAR:
+        raise DeskDFTError("overlap matrix singular after linear-dependence drop")
     return OrbitalSolution(C=C[:, :m].astype(dtype), epsilon=eps[:m].astype(dtype), n_occ=n_occ)

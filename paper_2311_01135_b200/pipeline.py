@@ -14,9 +14,10 @@ batches in flight on the GPU at once: each in-flight batch is driven by its own 
 thread and CUDA stream, so one batch's integral stage overlaps another's SCF loop (plans
 never synchronize the host inside a fixed-iteration run).  Records are appended and the
 checkpoint rewritten (atomically) after every completed batch; `wall_ms` is the
-molecule's share of its batch's wall time.  Multi-GPU: one process per GPU, each labeling
-its round-robin shard (`rank`, `world`) into its own output file; `merge_outputs` joins
-them.  No collective is involved.
+molecule's share of its batch's wall time.  Multi-GPU: `run(..., devices=[0, 1, ...])`
+starts one process per GPU, each labeling its round-robin shard into its own output file,
+and merges them (`merge_outputs`); a caller that runs its own ranks passes `rank`/`world`.
+No collective is involved.
 """
 
 from __future__ import annotations
@@ -209,19 +210,34 @@ def _record(entry_id: str, smiles, r, opts: SCFOptions, basis_name: str, wall_ms
 
 def run(manifest: GeometryManifest, opts: SCFOptions, workers: int, out_path: str,
         basis_name: str = "sto-3g", resume: bool = False, *, batch_size: int = 256,
-        rank: int = 0, world: int = 1, device: int | None = None, _label=None) -> list:
+        rank: int = 0, world: int = 1, device: int | None = None, devices=None, _label=None,
+        _skip: frozenset = frozenset()) -> list:
     """Label every manifest entry once; append records to out_path as JSONL (pipeline.py:154-219).
 
-    `workers`: device batches in flight (>= 1).  `rank`/`world`: this process labels
-    entries[rank::world].  `_label` is a test seam with label_batches' signature."""
+    `workers`: device batches in flight per GPU (>= 1).  `devices`: CUDA device indices; with
+    more than one, this call labels the whole manifest on all of them - one process per GPU,
+    each labeling its round-robin shard into out_path.dev<k>, merged into out_path at the end
+    (the reference labels with one call too, pipeline.py:200-213).  `rank`/`world`: for a
+    caller that runs the ranks itself, this process labels entries[rank::world].  `_label` is
+    a test seam with label_batches' signature."""
     if workers < 1:
         raise DeskDFTError("workers must be >= 1")
     if batch_size < 1:
         raise DeskDFTError("batch_size must be >= 1")
+    if devices is not None:
+        devices = [int(d) for d in devices]
+        if not devices:
+            raise DeskDFTError("devices must name at least one device")
+        if len(devices) > 1:
+            if world != 1 or rank != 0:
+                raise DeskDFTError("devices= runs its own ranks: leave rank/world at their defaults")
+            return _run_devices(manifest, opts, workers, out_path, basis_name, resume, batch_size,
+                                devices, _label)
+        device = devices[0]
     ckpt_path = out_path + ".ckpt"
     done, kept = _resume_state(out_path, ckpt_path, resume)
     records = [DatasetRecord.from_json(x) for x in kept]
-    todo = [e for e in manifest.entries[rank::world] if e.id not in done]
+    todo = [e for e in manifest.entries[rank::world] if e.id not in done and e.id not in _skip]
     if not todo:
         return records
     basis = load_basis(basis_name)
@@ -259,6 +275,43 @@ def run(manifest: GeometryManifest, opts: SCFOptions, workers: int, out_path: st
                 fh.write("".join(x + "\n" for x in lines))
         _atomic_write(ckpt_path, "".join(x + "\n" for x in sorted(done)))
     return records
+
+
+def _device_worker(manifest, opts, workers, path, basis_name, resume, batch_size, rank, world, device,
+                   skip, label):
+    run(manifest, opts, workers, path, basis_name, resume, batch_size=batch_size, rank=rank, world=world,
+        device=device, _label=label, _skip=skip)
+
+
+def _run_devices(manifest, opts, workers, out_path, basis_name, resume, batch_size, devices, label) -> list:
+    """One spawned process per device, shard k = entries[k::G] (no collective: the molecules
+    are independent); every shard checkpoints into its own file, so a killed run resumes per
+    shard, and the shards are merged into out_path (records already in it first)."""
+    import multiprocessing as mp
+
+    done, _ = _resume_state(out_path, out_path + ".ckpt", resume)
+    g = len(devices)
+    paths = [f"{out_path}.dev{k}" for k in range(g)]
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_device_worker,
+                         args=(manifest, opts, workers, paths[k], basis_name, resume, batch_size, k, g,
+                               devices[k], frozenset(done), label))
+             for k in range(g)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join()
+    bad = [k for k, p in enumerate(procs) if p.exitcode != 0]
+    if bad:
+        raise DeskDFTError(f"labeling process(es) for device(s) {[devices[k] for k in bad]} failed "
+                           f"(exit codes {[procs[k].exitcode for k in bad]}); completed shards are kept "
+                           "for resume=True")
+    recs = merge_outputs([out_path] + [p for p in paths if os.path.exists(p)], out_path)
+    for p in paths:
+        for f in (p, p + ".ckpt"):
+            if os.path.exists(f):
+                os.remove(f)
+    return recs
 
 
 def merge_outputs(paths: list, out_path: str) -> list:

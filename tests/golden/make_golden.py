@@ -100,6 +100,16 @@ def small_fixtures(b):
             if name == "dh2o" and lvl == 0:
                 arrs["dh2o_phi0"] = aov.phi
                 arrs["dh2o_gphi0"] = aov.grad_phi
+        # f32 operators (the reference's f32 working dtype): f32-stored ERIs
+        # and f32 rho through build_jk; f32 AO values and rho through xc_matrix at level 0
+        rho32 = rho.astype(np.float32)
+        J32, K32 = R_int.build_jk(R_int.eri_packed(ao, screen_eps=0.0, dtype=np.float32), rho32)
+        arrs[f"{name}_J32"] = J32
+        arrs[f"{name}_K32"] = K32
+        g0 = R_xc.build_grid(m, level=0)
+        x32 = R_xc.xc_matrix(g0, R_xc.eval_ao(ao, g0, dtype=np.float32), rho32)
+        rec["exc0_f32"] = x32.E_xc
+        arrs[f"{name}_vxc0_f32"] = x32.V_xc
         sol = R_roothaan(ints.V + ints.T, ints.S)
         arrs[f"{name}_core_eps"] = sol.epsilon
         out_json[name] = rec
@@ -175,7 +185,28 @@ def synth_eri_fixture(b):
     J, K = R_int.build_jk(e0, rho)
     arrs = {"syneri_ijkl": np.stack([e0.i[pick], e0.j[pick], e0.k[pick], e0.l[pick]]).astype(np.int32),
             "syneri_v": e0.values[pick], "syneri_rho": rho, "syneri_J": J, "syneri_K": K}
+    # the f32 operators at full molecule size: J/K over the f32 store, V_xc from f32 AO values
+    rho32 = rho.astype(np.float32)
+    J32, K32 = R_int.build_jk(R_int.eri_packed(ao, screen_eps=0.0, dtype=np.float32), rho32)
+    arrs["syneri_J32"], arrs["syneri_K32"] = J32, K32
+    g0 = R_xc.build_grid(rm, level=0)
+    for tag, dt in (("64", np.float64), ("32", np.float32)):
+        x = R_xc.xc_matrix(g0, R_xc.eval_ao(ao, g0, dtype=dt), rho.astype(dt))
+        rec[f"exc0_{tag}"] = x.E_xc
+        arrs[f"syneri_vxc0_{tag}"] = x.V_xc
     return rec, arrs
+
+
+def dump_fixtures(b):
+    """Binary dumps written by the reference (integrals.py:248-291): the packed ERIs of the
+    distorted water in f64 and f32, and its S/T/V set -> tests/golden/dumps/*.bin."""
+    d = os.path.join(HERE, "dumps")
+    os.makedirs(d, exist_ok=True)
+    m = R_parse(SMALL_XYZ["dh2o"])
+    ao = R_expand(m, b)
+    R_int.dump_packed(R_int.eri_packed(ao), os.path.join(d, "dh2o_eri_f64.bin"))
+    R_int.dump_packed(R_int.eri_packed(ao, dtype=np.float32), os.path.join(d, "dh2o_eri_f32.bin"))
+    R_int.dump_integral_set(R_int.one_electron(ao, m), os.path.join(d, "dh2o_stv.bin"))
 
 
 def study_records(k=48):
@@ -216,6 +247,7 @@ def main():
         rec, a2 = synth_eri_fixture(b)
         out["synth_eri"] = rec
         arrs.update(a2)
+    dump_fixtures(b)
     out["study"] = study_records()
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(out, fh, indent=1)

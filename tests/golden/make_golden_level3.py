@@ -24,7 +24,7 @@ OPTS = {"precision": "f64", "grid_level": 3, "convergence_std": 1e-9, "max_itera
 
 
 def main():
-    n = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 32
     mols = synth.batch(n, 11, seed=11)
     jobs = [(list(m.atomic_numbers), m.positions.tolist(), OPTS) for m in mols]
     with ProcessPoolExecutor(max_workers=min(n, os.cpu_count() or 1)) as ex:

@@ -72,3 +72,61 @@ def test_gloo_world2_sharded_queue():
     ref = [nuclear_repulsion(m) for m in synth.batch(n, 3, seed=3)]
     np.testing.assert_array_equal(np.array(merged), np.array(ref))
     assert tmax == 2.0
+
+
+def test_relaunch_torchrun_gloo():
+    """The launch path of `bench.py --gpus N` (relaunch under torch.distributed.run, one
+    process per rank, 127.0.0.1 rendezvous) with world size 2 on gloo: every rank labels
+    its shard, the max-over-ranks time and the molecule sum come back to rank 0."""
+    import json
+    import subprocess
+    import sys
+
+    from paper_2311_01135_b200.launch import torchrun_argv
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    cmd = torchrun_argv(2, os.path.join(here, "dist_probe.py"), [])
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["world"] == 2 and d["max"] == 2.0 and d["n"] == 5
+    ref = sum(nuclear_repulsion(m) for m in synth.batch(5, 3, seed=3))
+    assert abs(d["enn"] - ref) < 1e-9 * abs(ref)
+    del sys
+
+
+def test_bench_gpus_flag_relaunches(monkeypatch):
+    """`bench.py --gpus 2` started as a plain process re-executes itself under torchrun with
+    two ranks instead of running one (the round-1 bug: --gpus was parsed and ignored)."""
+    import importlib.util
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    seen = {}
+
+    def fake_relaunch(n, script, argv, env=None):
+        seen["n"], seen["script"], seen["argv"] = n, script, argv
+        return 0
+
+    import paper_2311_01135_b200.launch as launch
+
+    monkeypatch.setattr(launch, "relaunch_torchrun", fake_relaunch)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        monkeypatch.delenv(k, raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "2", "--steps", "3"])
+    with pytest.raises(SystemExit) as ex:
+        bench.main()
+    assert ex.value.code == 0
+    assert seen["n"] == 2 and seen["script"].endswith("bench.py") and seen["argv"] == ["--gpus", "2", "--steps", "3"]
+    # under a launcher whose world size disagrees with --gpus the bench refuses to run
+    monkeypatch.setenv("WORLD_SIZE", "1")
+    monkeypatch.setenv("RANK", "0")
+    with pytest.raises(SystemExit) as ex2:
+        bench.main()
+    assert "launcher started 1" in str(ex2.value.code)

@@ -201,3 +201,40 @@ def test_variance_stats(tmp_path):
     assert open(p).read().startswith("smiles,gap_std_ev\nC,")
     empty = variance_stats([], bins=3)
     assert empty.per_smiles_std == {} and empty.hist_counts == [0, 0, 0]
+
+
+def test_run_on_several_devices_merges_shards(tmp_path, monkeypatch):
+    """run(devices=[0, 1]): one spawned process per device labels entries[k::2] into its own
+    file; the merged output holds every entry once and equals a single-process run."""
+    from helpers.cpu_label import oracle_label
+
+    man = _manifest(tmp_path)
+    log = tmp_path / "devices.log"
+    monkeypatch.setenv("QM1B_TEST_DEVICE_LOG", str(log))
+    out2 = str(tmp_path / "two.jsonl")
+    recs2 = run(man, FAST, 1, out2, devices=[0, 1], batch_size=1, _label=oracle_label)
+    out1 = str(tmp_path / "one.jsonl")
+    recs1 = run(man, FAST, 1, out1, batch_size=1, _label=oracle_label)
+    a = {r.id: r for r in recs2}
+    b = {r.id: r for r in recs1}
+    assert set(a) == set(b) == {e.id for e in man.entries}
+    assert all(records_equal(a[k], b[k]) for k in a)
+    assert {r.id for r in load_records(out2)} == set(a)
+    assert sorted(open(out2 + ".ckpt").read().split()) == sorted(a)
+    assert not any(p.name.startswith("two.jsonl.dev") for p in tmp_path.iterdir())   # shards merged away
+    seen = [ln.split() for ln in log.read_text().splitlines()]
+    by_dev = {d: {i for dd, i in seen if dd == d} for d, _ in seen}
+    ids = [e.id for e in man.entries]
+    assert by_dev["0"] >= set(ids[0::2]) and by_dev["1"] >= set(ids[1::2])
+
+
+def test_run_on_several_devices_failure_keeps_shards(tmp_path):
+    from helpers.cpu_label import failing_label, oracle_label
+
+    man = _manifest(tmp_path)
+    out = str(tmp_path / "r.jsonl")
+    with pytest.raises(DeskDFTError, match="device"):
+        run(man, FAST, 1, out, devices=[0, 1], batch_size=1, _label=failing_label)
+    assert os.path.exists(out + ".dev0")                 # the healthy shard is kept for resume
+    recs = run(man, FAST, 1, out, devices=[0, 1], batch_size=1, resume=True, _label=oracle_label)
+    assert {r.id for r in recs} == {e.id for e in man.entries}
