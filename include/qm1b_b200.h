@@ -158,6 +158,11 @@ int dftb_diis(const double *F, const double *E, int32_t m, int32_t n, double *ou
 int dftb_plan_stage_times(const dftb_plan *plan, double *ms, int n);
 int dftb_plan_launch_count(const dftb_plan *plan, int64_t *count);
 int dftb_plan_set_timing(dftb_plan *plan, int enable);
+/* enable != 0: every SCF iteration diagonalises F' and stores C (the host iteration_callback
+ * path, scf.py:188-189, observes C each iteration).  Default 0: iterations before the last form
+ * the density projector by trace-correcting purification and only the last one (or the one
+ * that converges) diagonalises - the returned orbitals and eigenvalues are the same. */
+int dftb_plan_set_full_eig(dftb_plan *plan, int enable);
 /* Measured-peak helper: FP64 / FP32 FMA throughput microbenchmark (TFLOP/s). */
 int dftb_fma_peak(int fp64, double *tflops, void *stream);
 /* Kernel-level timing for roofline reporting: re-runs the J/K digestion and the XC

@@ -97,6 +97,7 @@ SIGNATURES = {
     "dftb_plan_stage_times": (ctypes.c_int, [ctypes.c_void_p, c_f64p, ctypes.c_int]),
     "dftb_plan_launch_count": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
     "dftb_plan_set_timing": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "dftb_plan_set_full_eig": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "dftb_fma_peak": (ctypes.c_int, [ctypes.c_int, c_f64p, ctypes.c_void_p]),
     "dftb_plan_kernel_times": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, c_f64p, c_f64p, ctypes.c_void_p]),
 }

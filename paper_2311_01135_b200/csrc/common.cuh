@@ -127,6 +127,9 @@ struct DevBatch {
     // per-molecule scalars
     double *enn, *hist, *comp, *Bmat, *eps;
     int *nmo, *ring_n, *ring_head, *done, *conv, *iters, *status;
+    int *cpv;                 // [n_mol] Cp holds the previous iteration's eigenvectors (warm start valid)
+    int *puri;                // [n_mol] purification sweeps of the last non-final iteration (diagnostics)
+    int full_eig;             // 1: eigendecomposition every iteration (host callback path)
     const double *boys;       // [BOYS_NT*BOYS_NCOL]
     int max_it;
     long long *dbg;           // [n_mol*16] phase cycle counters (diagnostics)

@@ -367,6 +367,261 @@ __global__ void __launch_bounds__(32 * jk_warps<NB>(), NB > 64 ? 2 : NB > 32 ? 3
         }
 }
 
+// ---------------------------------------------------------------------------- f32 build
+// The f32 build stores the ERI values and the density in f32 (the reference's f32 working
+// dtype, integrals.py:171, scf.py:169-174), so every product v * rho of the digestion is a
+// product of two f32 numbers.  k_jk32 forms those products on the packed FP32 pipe (FFMA2,
+// two lanes per instruction) in short f32 partial sums - four products per tile row / column
+// for K and J_P, one slab of rows for J_Q - and accumulates the partials in f64.  Relative to
+// the reference's exact f64 products that adds a rounding of ~2^-24 per partial, the size of
+// the f32 rounding already in every stored value.  Removes the per-element f32 -> f64
+// conversions (XU pipe) and DFMA of the f64 formulation; the digestion plan is the same as
+// k_jk's (one warp per row, lane group per 4-block a, A + 1 tile visits per block).
+template <int NB, int WARPS>
+struct JKPlan32 {
+    static constexpr int THREADS = 32 * WARPS;
+    static constexpr int AMAX = NB / 4;
+    static constexpr int LMAX = 8 * AMAX * (AMAX + 1);          // f32 elements of the longest row
+    static constexpr size_t row_bytes = (size_t)LMAX * 4;
+    // rho f32 [NB][NB] + J_Q accumulators f64 [LMAX] + G_i reduction [THREADS][4] f64
+    static constexpr size_t fixed = 128 + 4 * (size_t)NB * NB + 8 * (size_t)LMAX + 32 * (size_t)THREADS;
+    static constexpr size_t cap = 227 * 1024;
+    static constexpr int ctas(size_t bytes) { return (int)((228 * 1024) / (bytes + 1024)); }
+    static constexpr int NBUF =
+        fixed + 2 * WARPS * row_bytes <= cap && !(ctas(fixed + WARPS * row_bytes) > ctas(fixed + 2 * WARPS * row_bytes))
+            ? 2 : 1;
+    static constexpr int CR = fixed + NBUF * WARPS * row_bytes <= cap ? WARPS : WARPS / 2;
+    static constexpr size_t bytes = fixed + NBUF * CR * row_bytes;
+    static_assert(bytes <= cap, "J/K bucket does not fit in shared memory");
+};
+template <int NB> constexpr int jk32_warps() { return NB > 64 ? 8 : 4; }
+
+// rho f32 row-major, stride NB, 16-byte chunks XOR-swizzled by the row's 4-block (the
+// lanes of a warp read the same column block of rows in different 4-blocks)
+// (XOR over the low 3 chunk-index bits when a row holds a multiple of 8 chunks, else 2, so
+// the permutation stays inside the row)
+template <int NB>
+__device__ __forceinline__ int sw32key(int r) { return (r >> 2) & ((NB / 4) % 8 == 0 ? 7 : 3); }
+template <int NB>
+__device__ __forceinline__ int rsw32(int r, int c) {
+    return r * NB + (((c >> 2) ^ sw32key<NB>(r)) << 2) + (c & 3);
+}
+__device__ __forceinline__ float4 lds4(const float *p) { return *reinterpret_cast<const float4 *>(p); }
+
+template <int NB>
+__global__ void __launch_bounds__(32 * jk32_warps<NB>(), NB > 64 ? 1 : 3) k_jk32(DevBatch b, const int *ctas) {
+    constexpr int WARPS = jk32_warps<NB>();
+    using PL = JKPlan32<NB, WARPS>;
+    constexpr int THREADS = PL::THREADS, LMAX = PL::LMAX, NBUF = PL::NBUF, CR = PL::CR;
+    constexpr int KU = (LMAX / 4 + THREADS - 1) / THREADS;      // 16-byte units per thread
+    extern __shared__ __align__(128) unsigned char jsm[];
+    uint64_t *bar = (uint64_t *)jsm;
+    float *rho = (float *)(jsm + 128);                          // [NB][NB] swizzled, zero padded
+    double *jq = (double *)(rho + NB * NB);                     // [LMAX] J_Q by ket position
+    double *gred = jq + LMAX;                                   // [THREADS][4]
+    float *stage = (float *)(gred + 4 * THREADS);               // [NBUF][CR * LMAX]
+    const int cta = ctas[blockIdx.x];
+    const int m = b.jk_mol[cta];
+    if (b.done[m]) return;
+    const int N = b.m_nao[m];
+    const int64_t npp = tri(N);
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    const float *eri = (const float *)b.eri + b.m_eri0[m];
+    const int i0 = b.jk_i0[cta], i1 = b.jk_i1[cta];
+    int pi = i1 - 1, pj = 0;
+    auto issue = [&](int slot) {
+        const int nr = min(CR, pi + 1 - pj);
+        const int64_t L = eri_rowlen(pi);
+        bulk_copy(stage + (size_t)slot * CR * LMAX, eri + eri_row(pi, pj), (uint32_t)(nr * L * 4), bar + slot);
+        pj += CR;
+        if (pj > pi) { --pi; pj = 0; }
+    };
+    if (tid == 0) {
+        for (int k = 0; k < NBUF; ++k) mbar_init(bar + k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int k = 0; k < NBUF && pi >= i0; ++k) issue(k);
+    }
+    const double *rg = b.rho + b.m_mat0[m];
+    for (int t = tid; t < NB * NB; t += THREADS) {
+        const int r = t / NB, c = t % NB;
+        rho[rsw32<NB>(r, c)] = (r < N && c < N) ? (float)rg[r * N + c] : 0.f;   // f32-exact in this build
+    }
+    for (int t = tid; t < LMAX; t += THREADS) jq[t] = 0.0;
+    // per-CTA exchange partial (see k_jk)
+    double *Gp = b.Gpart + b.m_G0[m] + (int64_t)(cta - b.m_jkcta0[m]) * N * N;
+    for (int t = tid; t < N * N; t += THREADS) Gp[t] = 0.0;
+    __syncthreads();
+    double *Jp = b.Jpart + b.m_Jp0[m];
+    int chunk = 0;
+    for (int i = i1 - 1; i >= i0; --i) {
+        const int A = (i >> 2) + 1;
+        const int S = A <= 1 ? 32 : A <= 2 ? 16 : A <= 4 ? 8 : A <= 8 ? 4 : A <= 16 ? 2 : 1;
+        const int a = lane / S, s = lane % S;
+        const bool lane_ok = a < A;
+        const float *rhoA = rho + 4 * a * NB, *rhoI = rho + i * NB;
+        const int64_t L = eri_rowlen(i);
+        const int units = (int)(L / 4);
+        double gi[4] = {0, 0, 0, 0};
+        float2 jacc[KU][2];                                     // J_Q partials of this slab (f32)
+#pragma unroll
+        for (int k = 0; k < KU; ++k) jacc[k][0] = jacc[k][1] = make_float2(0.f, 0.f);
+        for (int j0 = 0; j0 <= i; j0 += CR, ++chunk) {
+            const int slot = chunk % NBUF;
+            const float *cbuf = stage + (size_t)slot * CR * LMAX;
+            mbar_wait(bar + slot, (uint32_t)((chunk / NBUF) & 1));
+            const int j = j0 + w;
+            if (w < CR && j <= i) {                             // warp-uniform
+                const float *row = cbuf + (int64_t)w * L;
+                const float *rhoJ = rho + j * NB;
+                double oJ[4] = {0, 0, 0, 0}, oI[4] = {0, 0, 0, 0}, jp = 0.0;
+                if (lane_ok) {
+                    for (int q = s; q <= A; q += S) {
+                        const bool rp = q <= a;
+                        const int ta = rp ? a : q - 1, tb = rp ? q : a;   // tile (ta, tb)
+                        const int beta = rp ? q : q - 1;                  // rho block of the product
+                        const float *tp = row + 16 * (tri32(ta) + tb);
+                        float tf[16];
+                        {
+                            const float4 r0 = lds4(tp), r1 = lds4(tp + 4), r2 = lds4(tp + 8), r3 = lds4(tp + 12);
+                            tf[0] = r0.x; tf[1] = r0.y; tf[2] = r0.z; tf[3] = r0.w;
+                            tf[4] = r1.x; tf[5] = r1.y; tf[6] = r1.z; tf[7] = r1.w;
+                            tf[8] = r2.x; tf[9] = r2.y; tf[10] = r2.z; tf[11] = r2.w;
+                            tf[12] = r3.x; tf[13] = r3.y; tf[14] = r3.z; tf[15] = r3.w;
+                        }
+                        if (ta == tb) { tf[0] *= 0.5f; tf[5] *= 0.5f; tf[10] *= 0.5f; tf[15] *= 0.5f; }
+                        float t[16];
+#pragma unroll
+                        for (int r = 0; r < 4; ++r)
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) t[4 * r + c] = rp ? tf[4 * r + c] : tf[4 * c + r];
+                        const float4 vj = lds4(rhoJ + ((beta ^ sw32key<NB>(j)) << 2));
+                        const float4 vi = lds4(rhoI + ((beta ^ sw32key<NB>(i)) << 2));
+                        const float2 u[4] = {make_float2(vj.x, vi.x), make_float2(vj.y, vi.y),
+                                             make_float2(vj.z, vi.z), make_float2(vj.w, vi.w)};
+                        // (T rho_j, T rho_i) per result row: one FFMA2 per product pair
+                        float2 o2[4];
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+                            for (int c = 0; c < 4; ++c)
+                                acc = __ffma2_rn(make_float2(t[4 * r + c], t[4 * r + c]), u[c], acc);
+                            o2[r] = acc;
+                        }
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            oJ[r] += (double)o2[r].x;
+                            oI[r] += (double)o2[r].y;
+                        }
+                        if (rp) {                               // J_P: row-part tiles only
+                            const int key = sw32key<NB>(4 * a);
+                            float2 d2 = make_float2(0.f, 0.f);
+#pragma unroll
+                            for (int r = 0; r < 4; ++r) {
+                                const float4 x = lds4(rhoA + r * NB + ((beta ^ key) << 2));
+                                d2 = __ffma2_rn(make_float2(t[4 * r], t[4 * r + 1]), make_float2(x.x, x.y), d2);
+                                d2 = __ffma2_rn(make_float2(t[4 * r + 2], t[4 * r + 3]), make_float2(x.z, x.w), d2);
+                            }
+                            jp += (double)d2.x + (double)d2.y;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) gi[u] = fma(2.0, oJ[u], gi[u]);
+                for (int o = 1; o < S; o <<= 1)
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) oI[u] += shfl_x(oI[u], o);
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) jp += shfl_x(jp, o);
+                const double vp = (double)row[eri_ket(i, j)];
+                const double rjI = rho[rsw32<NB>(j, i)], rjJ = rho[rsw32<NB>(j, j)];
+                const double riI = rho[rsw32<NB>(i, i)], riJ = rho[rsw32<NB>(i, j)];
+                if (lane_ok && s == 0) {
+                    double *Gj = Gp + (int64_t)j * N;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int t = 4 * a + u;
+                        double gJ = 2.0 * oI[u];
+                        if (t == j) { gi[u] -= vp * rjI; gJ -= vp * riI; }
+                        else if (t == i) { gi[u] -= vp * rjJ; gJ -= vp * riJ; }
+                        if (j < i && t <= i) atomicAdd(Gj + t, gJ);   // RED, order fixed by the chunk barriers
+                    }
+                }
+                if (lane == 0) Jp[tri(i) + j] = 2.0 * jp - vp * riJ * (i != j ? 2.0 : 1.0);
+            }
+            // ---- J_Q += v_PQ rho~_P over the chunk's rows (thread-owned 16-byte units, f32)
+            const int nr = min(CR, i + 1 - j0);
+            for (int rr = 0; rr < nr; ++rr) {
+                const int jj = j0 + rr;
+                const float wgt = rho[rsw32<NB>(i, jj)] * (i != jj ? 2.f : 1.f);   // exact
+                const float2 w2 = make_float2(wgt, wgt);
+                const float *rowp = cbuf + (int64_t)rr * L;
+#pragma unroll
+                for (int k = 0; k < KU; ++k) {
+                    const int u = tid + k * THREADS;
+                    if (u < units) {
+                        const float4 v = lds4(rowp + 4 * u);
+                        jacc[k][0] = __ffma2_rn(make_float2(v.x, v.y), w2, jacc[k][0]);
+                        jacc[k][1] = __ffma2_rn(make_float2(v.z, v.w), w2, jacc[k][1]);
+                    }
+                }
+            }
+            __syncthreads();                           // chunk consumed
+            if (tid == 0 && pi >= i0) issue(slot);
+        }
+        // ---- slab end: J_Q partials into the f64 accumulators; G_i fixed-order sums
+#pragma unroll
+        for (int k = 0; k < KU; ++k) {
+            const int u = tid + k * THREADS;
+            if (u < units) {
+                double2 *q2 = reinterpret_cast<double2 *>(jq + 4 * u);
+                double2 x = q2[0], y = q2[1];
+                x.x += (double)jacc[k][0].x; x.y += (double)jacc[k][0].y;
+                y.x += (double)jacc[k][1].x; y.y += (double)jacc[k][1].y;
+                q2[0] = x;
+                q2[1] = y;
+            }
+        }
+        for (int o = 1; o < S; o <<= 1)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) gi[u] += shfl_x(gi[u], o);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) gred[tid * 4 + u] = gi[u];
+        __syncthreads();
+        if (tid < A) {                                 // thread tid handles block tid
+            double *Gi = Gp + (int64_t)i * N;
+            for (int u = 0; u < 4; ++u) {
+                const int t = 4 * tid + u;
+                if (t > i) break;
+                double v = 0.0;
+                for (int ww = 0; ww < CR; ++ww) v += gred[(ww * 32 + tid * S) * 4 + u];
+                atomicAdd(Gi + t, v);
+            }
+        }
+        __syncthreads();
+    }
+    // ---- this CTA's J_Q partial, every Q of the molecule written once
+    const int local = cta - b.m_jkcta0[m];
+    double *Js = Jp + (int64_t)(1 + local) * npp;
+    const int64_t Lm = eri_rowlen(N - 1);
+    for (int e = tid; e < Lm; e += THREADS) {
+        const int tau = e >> 4;
+        int a = (int)((sqrt(8.0 * (double)tau + 1.0) - 1.0) * 0.5);
+        while (tri(a + 1) <= tau) ++a;
+        while (tri(a) > tau) --a;
+        const int bb = tau - (int)tri(a);
+        const int kk = 4 * a + ((e >> 2) & 3), ll = 4 * bb + (e & 3);
+        if (kk < N && ll <= kk) Js[tri(kk) + ll] = jq[e];
+    }
+}
+
+template <int NB>
+static void launch_bucket32(const DevBatch &b, const int *ctas, int n, cudaStream_t s) {
+    using PL = JKPlan32<NB, jk32_warps<NB>()>;
+    smem_optin((const void *)k_jk32<NB>);
+    k_jk32<NB><<<n, PL::THREADS, PL::bytes, s>>>(b, ctas);
+}
+
 template <typename ST, int NB>
 static void launch_bucket(const DevBatch &b, const int *ctas, int n, cudaStream_t s) {
     const size_t sm = JKPlan<ST, NB>::bytes;
@@ -393,8 +648,22 @@ static void launch_jk_t(const DevBatch &b, const int *bucket_ctas, const int *bu
 // bucket_ctas: device array of CTA indices grouped by AO-count bucket; bucket_n: host counts [6]
 int launch_jk(const DevBatch &b, const int *bucket_ctas, const int *bucket_n, cudaStream_t s) {
     if (b.n_jk_cta == 0) return 0;
-    if (b.eri64) launch_jk_t<double>(b, bucket_ctas, bucket_n, s);
-    else launch_jk_t<float>(b, bucket_ctas, bucket_n, s);
+    if (b.eri64) {
+        launch_jk_t<double>(b, bucket_ctas, bucket_n, s);
+    } else {
+        const int *c = bucket_ctas;
+        if (bucket_n[0]) launch_bucket32<16>(b, c, bucket_n[0], s);
+        c += bucket_n[0];
+        if (bucket_n[1]) launch_bucket32<32>(b, c, bucket_n[1], s);
+        c += bucket_n[1];
+        if (bucket_n[2]) launch_bucket32<48>(b, c, bucket_n[2], s);
+        c += bucket_n[2];
+        if (bucket_n[3]) launch_bucket32<64>(b, c, bucket_n[3], s);
+        c += bucket_n[3];
+        if (bucket_n[4]) launch_bucket32<80>(b, c, bucket_n[4], s);
+        c += bucket_n[4];
+        if (bucket_n[5]) launch_bucket32<96>(b, c, bucket_n[5], s);
+    }
     int k = 0;
     for (int i = 0; i < 6; ++i) k += bucket_n[i] > 0;
     return k;

@@ -520,8 +520,8 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
     const size_t o_Bmat = L.add<double>((size_t)nm * DIIS_MAX * DIIS_MAX);
     const size_t o_eps = L.add<double>((size_t)nm * NMAX);
     const size_t o_dbg = L.add<long long>((size_t)nm * 16);
-    size_t o_ints[7];
-    for (int k = 0; k < 7; ++k) o_ints[k] = L.add<int>(nm);
+    size_t o_ints[9];
+    for (int k = 0; k < 9; ++k) o_ints[k] = L.add<int>(nm);
     const int eri64 = !opts->precision || ERI64_F32;
     const int esz = eri64 ? 8 : 4;
     p->eri_off = L.add<char>((size_t)eri0[nm] * esz);
@@ -623,6 +623,9 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
     d.nmo = PTR(int, o_ints[0]); d.ring_n = PTR(int, o_ints[1]); d.ring_head = PTR(int, o_ints[2]);
     d.done = PTR(int, o_ints[3]); d.conv = PTR(int, o_ints[4]); d.iters = PTR(int, o_ints[5]);
     d.status = PTR(int, o_ints[6]);
+    d.cpv = PTR(int, o_ints[7]);
+    d.puri = PTR(int, o_ints[8]);
+    d.full_eig = 0;
     d.max_it = maxit;
     d.dbg = PTR(long long, o_dbg);
 #undef PTR
@@ -658,6 +661,12 @@ static int setup_stage(dftb_plan *p, cudaStream_t st, bool screened) {
     launch_eri(d, p->cls_tot, eps, 1e-3 * eps, st, &nl);
     p->launches += 2 + 3 + 1 + nl;
     CK(cudaGetLastError());
+    return 0;
+}
+
+int dftb_plan_set_full_eig(dftb_plan *p, int enable) {
+    if (!p) return fail(DFTB_EINVAL, "null plan");
+    p->d.full_eig = enable != 0;
     return 0;
 }
 

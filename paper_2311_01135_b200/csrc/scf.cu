@@ -354,6 +354,102 @@ __device__ void sort_dv(int n, const Arena &ar) {
     __syncthreads();
 }
 
+// ---------------------------------------------------------------------------- purification
+// Density projector without an eigendecomposition: the SCF needs the orbitals only to form
+// rho = 2 C_occ C_occ^T (scf.py:68-74), i.e. the spectral projector of F' = X^T F X onto its
+// n_occ lowest eigenvectors, and the eigenvalues only after the last iteration (scf.py:202-210).
+// Trace-correcting purification (Niklasson, Phys. Rev. B 66, 155115 (2002)) builds that
+// projector from matrix squares alone: X0 = (hi I - F') / (hi - lo) maps the spectrum (inside
+// the Gershgorin bounds [lo, hi]) into [0, 1] with the occupied levels on top, and each step
+// replaces X by X^2 or 2X - X^2 - whichever trace lands closer to n_occ - which drives the
+// n_occ highest eigenvalues of X to 1 and the rest to 0 with the eigenvectors unchanged.  It
+// converges quadratically once the HOMO-LUMO gap is resolved; we stop two steps after the
+// idempotency error tr(X - X^2) = sum l(1 - l) falls below 1e-11, i.e. at round-off
+// (|l(1 - l)| < 1e-22).  One symmetric square per step (upper 4 x 4 tiles, Y in B) and two
+// CTA barriers: ~20-30 steps against the 3-10 Jacobi sweeps of N - 1 rotation steps each.
+// Returns false (the caller then diagonalises) if it has not converged after TC2_MAX steps,
+// e.g. for a vanishing gap, where the projector is not defined by the spectrum alone.
+constexpr int TC2_MAX = 100;
+
+__device__ bool cta_tc2(double *X, double *Y, int M, int nocc, const Arena &ar, int *nsteps) {
+    const int tid = threadIdx.x, nt = SCF_THREADS;
+    const int T = (M + 3) >> 2;                       // tiles per dimension
+    const int ntile = T * (T + 1) / 2;                // upper triangle (ta <= tb)
+    // spectral bounds (Gershgorin) and X0
+    double lo = -1e300, hi = -1e300;                  // lo holds -min
+    for (int i = tid; i < M; i += nt) {
+        double r = 0.0;
+        for (int j = 0; j < M; ++j)
+            if (j != i) r += fabs(X[i * M + j]);
+        lo = fmax(lo, -(X[i * M + i] - r));
+        hi = fmax(hi, X[i * M + i] + r);
+    }
+    block_max2(lo, hi, ar.red);
+    lo = -lo;
+    const double sc = 1.0 / (hi - lo);
+    for (int t = tid; t < M * M; t += nt) {
+        const int r = t / M, c = t - r * M;
+        X[t] = ((r == c ? hi : 0.0) - X[t]) * sc;
+    }
+    double tr = 0.0;
+    for (int i = tid; i < M; i += nt) tr += X[i * M + i];
+    tr = block_sum(tr, ar.red);                       // ends with a barrier: X0 complete
+    int extra = -1, k = 0;
+    bool ok = false;
+    for (; k < TC2_MAX; ++k) {
+        // Y = X X (X symmetric: Y_ij = sum_l X_li X_lj), upper tiles, mirrored on write
+        for (int u = tid; u < ntile; u += nt) {
+            int ta = 0, rem = u;
+            while (rem >= T - ta) { rem -= T - ta; ++ta; }
+            const int tb = ta + rem;
+            const int i0 = 4 * ta, j0 = 4 * tb;
+            double acc[4][4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+            for (int l = 0; l < M; ++l) {
+                const double *xr = X + l * M;
+                double xi[4], xj[4];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    xi[a] = i0 + a < M ? xr[i0 + a] : 0.0;
+                    xj[a] = j0 + a < M ? xr[j0 + a] : 0.0;
+                }
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) acc[a][c] = fma(xi[a], xj[c], acc[a][c]);
+            }
+            double dsum = 0.0;
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int i = i0 + a, j = j0 + c;
+                    if (i < M && j < M) {
+                        Y[i * M + j] = acc[a][c];
+                        Y[j * M + i] = acc[a][c];
+                        if (i == j) dsum += acc[a][c];
+                    }
+                }
+            if (ta == tb) ar.dv[ta] = dsum;
+        }
+        __syncthreads();
+        double tr2 = 0.0;
+        for (int a = 0; a < T; ++a) tr2 += ar.dv[a];    // same fixed order in every thread
+        const bool sq = fabs(tr2 - nocc) <= fabs(2.0 * tr - tr2 - nocc);
+        const double idem = tr - tr2;
+        for (int t = tid; t < M * M; t += nt) X[t] = sq ? Y[t] : 2.0 * X[t] - Y[t];
+        tr = sq ? tr2 : 2.0 * tr - tr2;
+        __syncthreads();
+        if (extra < 0 && fabs(idem) < 1e-11) extra = 0;
+        if (extra >= 0 && ++extra > 2) { ok = true; ++k; break; }
+    }
+    *nsteps = k;
+    return ok && fabs(tr - nocc) < 1e-6;
+}
+
 // ---------------------------------------------------------------------------- orthogonaliser
 __global__ void __launch_bounds__(SCF_THREADS, 2) k_orth(DevBatch b, int nm) {
     extern __shared__ __align__(16) unsigned char ssm[];
@@ -719,43 +815,84 @@ __global__ void __launch_bounds__(SCF_THREADS, 2) k_post(DevBatch b, PostArgs pa
         }
     }
     tick(3);
-    // (9) Roothaan: F' = X^T F X, Jacobi (warm start from previous C'), C = X C'
-    cta_gemm(S2, N, Fuse, N, false, X, N, false, N, M, N, 1.0, 0.0, ar);     // F X  (N x M, ld N)
-    cta_gemm(ar.A, M, X, N, true, S2, N, false, M, M, N, 1.0, 0.0, ar);      // X^T (F X)
-    const double *Ad = nullptr;
-    if (it >= 0) {
-        // warm start: Jacobi on C'^T F' C' with V = C' (previous eigenvectors)
-        cta_gemm(S1, M, ar.A, M, false, Cp, M, false, M, M, M, 1.0, 0.0, ar); // F' C'
-        cta_gemm(ar.A, M, Cp, M, true, S1, M, false, M, M, M, 1.0, 0.0, ar);  // C'^T F' C'
-        for (int t = tid; t < M * M; t += SCF_THREADS) ar.B[(t % M) * M + t / M] = Cp[t];   // V^T = C'^T
-    } else {
-        for (int t = tid; t < M * M; t += SCF_THREADS) ar.B[t] = (t / M == t % M) ? 1.0 : 0.0;
+    // convergence is decided before the solve: it depends on the energies alone (scf.py:198-200),
+    // and the last iteration is the one whose orbitals and eigenvalues are returned
+    if (tid == 0) {
+        int stop = 0, cv = 0;
+        if (it >= 0) {
+            stop = it + 1 >= b.max_it;
+            if (it + 1 >= 5) {
+                const double *hh = b.hist + (int64_t)m * b.max_it + it - 4;
+                double mean = 0.0;
+                for (int k = 0; k < 5; ++k) mean += hh[k];
+                mean /= 5.0;
+                double var = 0.0;
+                for (int k = 0; k < 5; ++k) var += (hh[k] - mean) * (hh[k] - mean);
+                if (sqrt(var / 5.0) < pa.conv_std) {
+                    cv = 1;
+                    stop = 1;
+                }
+            }
+        }
+        ar.scal[2] = stop;
+        ar.scal[3] = cv;
     }
     __syncthreads();
-    {
+    const bool last = ar.scal[2] != 0.0;
+    // (9) F' = X^T F X; orbitals (last iteration / callback path) or the density projector
+    cta_gemm(S2, N, Fuse, N, false, X, N, false, N, M, N, 1.0, 0.0, ar);     // F X  (N x M, ld N)
+    cta_gemm(ar.A, M, X, N, true, S2, N, false, M, M, N, 1.0, 0.0, ar);      // X^T (F X)
+    bool eig = last || b.full_eig;
+    if (!eig) {
+        int nst = 0;
+        if (cta_tc2(ar.A, ar.B, M, nocc, ar, &nst)) {
+            // rho_new = 2 X P' X^T
+            cta_gemm(S2, N, X, N, false, ar.A, M, false, N, M, M, 1.0, 0.0, ar);   // X P'  (N x M)
+            cta_gemm(S1, N, S2, N, false, X, N, true, N, N, M, 2.0, 0.0, ar);       // 2 (X P') X^T
+            if (tid == 0) { b.puri[m] = nst; b.cpv[m] = 0; }
+        } else {
+            eig = true;                               // no converged projector: diagonalise
+            if (tid == 0) b.puri[m] = -nst;
+            cta_gemm(ar.A, M, X, N, true, S2, N, false, M, M, N, 1.0, 0.0, ar);   // F' again
+        }
+        tick(4);
+    }
+    if (eig) {
+        const bool warm = b.cpv[m] != 0;
+        if (warm) {
+            // warm start: Jacobi on C'^T F' C' with V = C' (previous eigenvectors)
+            cta_gemm(S1, M, ar.A, M, false, Cp, M, false, M, M, M, 1.0, 0.0, ar); // F' C'
+            cta_gemm(ar.A, M, Cp, M, true, S1, M, false, M, M, M, 1.0, 0.0, ar);  // C'^T F' C'
+            for (int t = tid; t < M * M; t += SCF_THREADS) ar.B[(t % M) * M + t / M] = Cp[t];   // V^T = C'^T
+        } else {
+            for (int t = tid; t < M * M; t += SCF_THREADS) ar.B[t] = (t / M == t % M) ? 1.0 : 0.0;
+        }
+        __syncthreads();
         // f32 build: eigenvectors to f32 resolution (the reference's f32 path diagonalizes in
         // single precision, scf.py:86-98); f64 build: to 1e-13 of the largest |eigenvalue|
         int nsw = 0;
-        Ad = cta_jacobi(ar.A, ar.B, M, ar, &nsw, 30, b.prec ? 1e-8 : 1e-13);
+        const double *Ad = cta_jacobi(ar.A, ar.B, M, ar, &nsw, 40, b.prec ? 1e-8 : 1e-13);
         if (dbg && tid == 0) dbg[10] += nsw;
+        tick(4);
+        sort_eigs(Ad, M, ar);
+        tick(5);
+        for (int t = tid; t < M * M; t += SCF_THREADS) {
+            const int row = t / M, i = t % M;
+            Cp[row * M + ar.perm[i]] = ar.B[i * M + row];
+        }
+        for (int i = tid; i < M; i += SCF_THREADS) b.eps[(int64_t)m * NMAX + ar.perm[i]] = ar.dv[i];
+        __syncthreads();
+        cta_gemm(C, N, X, N, false, Cp, M, false, N, M, M, 1.0, 0.0, ar);         // C = X C' (N x M)
+        // rho_new = 2 C_occ C_occ^T
+        cta_gemm(S1, N, C, N, false, C, N, true, N, N, nocc, 2.0, 0.0, ar);
+        if (tid == 0) b.cpv[m] = 1;
     }
-    tick(4);
-    sort_eigs(Ad, M, ar);
-    tick(5);
-    for (int t = tid; t < M * M; t += SCF_THREADS) {
-        const int row = t / M, i = t % M;
-        Cp[row * M + ar.perm[i]] = ar.B[i * M + row];
-    }
-    for (int i = tid; i < M; i += SCF_THREADS) b.eps[(int64_t)m * NMAX + ar.perm[i]] = ar.dv[i];
-    __syncthreads();
-    cta_gemm(C, N, X, N, false, Cp, M, false, N, M, M, 1.0, 0.0, ar);         // C = X C' (N x M)
-    // rho_new = 2 C_occ C_occ^T (+ damping when the next iteration is pre-DIIS)
-    cta_gemm(S2, N, C, N, false, C, N, true, N, N, nocc, 2.0, 0.0, ar);
+    // (+ damping when the next iteration is pre-DIIS)
     const int nxt = it + 1;
     const bool damp = nxt > 0 && nxt < pa.diis_start;
     const double d = pa.damping;
     for (int t = tid; t < N * N; t += SCF_THREADS) {
-        double v = S2[t];
+        double v = S1[t];
         if (damp) v = d * rho[t] + (1.0 - d) * v;
         if (b.prec) v = (double)(float)v;
         rho[t] = v;
@@ -764,20 +901,8 @@ __global__ void __launch_bounds__(SCF_THREADS, 2) k_post(DevBatch b, PostArgs pa
     if (dbg && tid == 0) dbg[11] += 1;
     if (tid == 0 && it >= 0) {
         b.iters[m] = it + 1;
-        bool stop = (it + 1 >= b.max_it);
-        if (it + 1 >= 5) {
-            const double *hh = b.hist + (int64_t)m * b.max_it + it - 4;
-            double mean = 0.0;
-            for (int k = 0; k < 5; ++k) mean += hh[k];
-            mean /= 5.0;
-            double var = 0.0;
-            for (int k = 0; k < 5; ++k) var += (hh[k] - mean) * (hh[k] - mean);
-            if (sqrt(var / 5.0) < pa.conv_std) {
-                b.conv[m] = 1;
-                stop = true;
-            }
-        }
-        if (stop) b.done[m] = 1;
+        if (ar.scal[3] != 0.0) b.conv[m] = 1;
+        if (last) b.done[m] = 1;
     }
 }
 

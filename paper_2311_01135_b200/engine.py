@@ -137,6 +137,10 @@ class Plan:
         _lib.check(self.lib.dftb_plan_jk(self.h, _lib.ptr(r), _lib.ptr(J), _lib.ptr(K), self.stream))
         return J, K
 
+    def set_full_eig(self, on: bool = True):
+        """Diagonalise every iteration (C available per iteration) instead of purifying."""
+        _lib.check(self.lib.dftb_plan_set_full_eig(self.h, 1 if on else 0))
+
     def set_timing(self, on: bool = True):
         _lib.check(self.lib.dftb_plan_set_timing(self.h, 1 if on else 0))
 

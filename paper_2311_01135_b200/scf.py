@@ -154,6 +154,7 @@ def scf(m: Molecule, b: BasisSet, opts: SCFOptions | None = None,
 def _scf_with_callback(m, b, opts, cb) -> SCFResult:
     """Slow path: one device iteration at a time, rho / C copied to the host for the callback."""
     with Plan([m], b, opts.engine()) as plan:
+        plan.set_full_eig(True)          # the callback observes C every iteration
         plan.begin()
         S = plan.get("S").astype(opts.dtype)
         n = int(plan.pk.mol_nao[0])
