@@ -113,6 +113,8 @@ def load(require_device: bool = True):
                               "(there is no CPU fallback)")
         lib = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
+            if _DEV_LIB and not hasattr(lib, name):
+                continue   # an older build under A/B: entry points it lacks stay unbound
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

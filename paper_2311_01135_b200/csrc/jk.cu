@@ -394,6 +394,9 @@ struct JKPlan32 {
     static constexpr size_t bytes = fixed + NBUF * CR * row_bytes;
     static_assert(bytes <= cap, "J/K bucket does not fit in shared memory");
 };
+#ifndef JK32
+#define JK32 1   // 0: the f32 build digests through k_jk<float> (f64 products) - A/B only
+#endif
 template <int NB> constexpr int jk32_warps() { return NB > 64 ? 8 : 4; }
 
 // rho f32 row-major, stride NB, 16-byte chunks XOR-swizzled by the row's 4-block (the
@@ -648,8 +651,9 @@ static void launch_jk_t(const DevBatch &b, const int *bucket_ctas, const int *bu
 // bucket_ctas: device array of CTA indices grouped by AO-count bucket; bucket_n: host counts [6]
 int launch_jk(const DevBatch &b, const int *bucket_ctas, const int *bucket_n, cudaStream_t s) {
     if (b.n_jk_cta == 0) return 0;
-    if (b.eri64) {
-        launch_jk_t<double>(b, bucket_ctas, bucket_n, s);
+    if (b.eri64 || !JK32) {
+        if (b.eri64) launch_jk_t<double>(b, bucket_ctas, bucket_n, s);
+        else launch_jk_t<float>(b, bucket_ctas, bucket_n, s);
     } else {
         const int *c = bucket_ctas;
         if (bucket_n[0]) launch_bucket32<16>(b, c, bucket_n[0], s);

@@ -625,7 +625,11 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
     d.status = PTR(int, o_ints[6]);
     d.cpv = PTR(int, o_ints[7]);
     d.puri = PTR(int, o_ints[8]);
+#ifdef FORCE_FULL_EIG
+    d.full_eig = 1;
+#else
     d.full_eig = 0;
+#endif
     d.max_it = maxit;
     d.dbg = PTR(long long, o_dbg);
 #undef PTR

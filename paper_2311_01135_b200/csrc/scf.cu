@@ -391,6 +391,7 @@ __device__ bool cta_tc2(double *X, double *Y, int M, int nocc, const Arena &ar, 
         const int r = t / M, c = t - r * M;
         X[t] = ((r == c ? hi : 0.0) - X[t]) * sc;
     }
+    __syncthreads();                                  // the diagonal below has other writers
     double tr = 0.0;
     for (int i = tid; i < M; i += nt) tr += X[i * M + i];
     tr = block_sum(tr, ar.red);                       // ends with a barrier: X0 complete

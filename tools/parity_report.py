@@ -22,6 +22,42 @@ def stats(d):
     return f"{d.mean():.4g}", f"{d.max():.4g}"
 
 
+SETTLED = 1e-5  # Ha: std of the reference f64 run's last five energies
+
+
+def config1_rows(b, raw_path=None):
+    """The bench's own configs[1] batch (synth.batch(256, 9, seed=1000)) vs the reference's
+    labels of it (tests/golden/config1_batch.json): f64 and f32 builds, split into molecules
+    whose reference f64 SCF settles in 20 fixed iterations (std(last 5 E) < SETTLED) and the
+    rest (still oscillating: the f32/f64 and device/reference differences there measure the
+    SCF's chaos, not the arithmetic)."""
+    c1 = json.load(open(os.path.join(ROOT, "tests", "golden", "config1_batch.json")))
+    recs = c1["molecules"]
+    mols = [Molecule(tuple(r["Z"]), np.array(r["pos_bohr"])) for r in recs]
+    settled = np.array([np.std(r["f64"]["last5"]) < SETTLED for r in recs])
+    out, raw = [], {"settled": settled.tolist()}
+    ours = {}
+    for prec in ("f64", "f32"):
+        rs = scf_batch(mols, b, SCFOptions(max_iterations=20, convergence_std=0.0, grid_level=0, precision=prec))
+        ours[prec] = np.array([(r.E_total, properties(r)["gap"]) for r in rs])
+    ref = {p: np.array([(r[p]["E_total"], r[p]["gap_ev"]) for r in recs]) for p in ("f64", "f32")}
+    for name, a, c in (("B200 f64 vs reference f64", ours["f64"], ref["f64"]),
+                       ("B200 f32 vs reference f64", ours["f32"], ref["f64"]),
+                       ("B200 f32 vs reference f32", ours["f32"], ref["f32"]),
+                       ("reference f32 vs reference f64 (its own spread)", ref["f32"], ref["f64"])):
+        de = (a[:, 0] - c[:, 0]) * HARTREE_TO_EV
+        dg = a[:, 1] - c[:, 1]
+        raw[name] = {"dE_ha": (a[:, 0] - c[:, 0]).tolist(), "dgap_ev": dg.tolist()}
+        for label, k in (("settled", settled), ("oscillating", ~settled)):
+            if k.any():
+                out.append(f"| configs[1] batch (bench input), level 0, 20 fixed it., {label} | {name} | "
+                           f"{int(k.sum())} | {' | '.join(stats(de[k]))} | {' | '.join(stats(dg[k]))} |")
+    if raw_path:
+        with open(raw_path, "w") as fh:
+            json.dump(raw, fh)
+    return out
+
+
 def main():
     g = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))
     b = load_basis("sto-3g")
@@ -58,11 +94,12 @@ def main():
         lines.append(f"| reference study (f64 records), level 1, conv 1e-4 | B200 {prec} vs reference f64 "
                      f"(iterations identical: {same_it}/{len(recs)}) | {len(recs)} | "
                      f"{' | '.join(stats(de))} | {' | '.join(stats(dg))} |")
+    lines.extend(config1_rows(b, os.environ.get("PARITY_RAW")))
     text = "\n".join(lines) + "\n"
     if len(sys.argv) > 1:
         with open(sys.argv[1], "w") as fh:
             fh.write("# Parity report (B200 build vs deskdft golden results)\n\n")
-            fh.write("Generated by `python tools/parity_report.py profiles/r1_parity_report.md` on a B200.\n\n")
+            fh.write(f"Generated by `python tools/parity_report.py {sys.argv[1]}` on a B200.\n\n")
             fh.write(text)
     print(text)
 
