@@ -324,8 +324,8 @@ def test_config5_shape_level3_convergence(gpu_lib, sto3g):
 @pytest.mark.slow
 def test_config5_level3_against_reference(gpu_lib, sto3g):
     """BASELINE configs[4] settings (11 heavy atoms, f64, grid level 3, converged to
-    std(last 5 E) < 1e-9, max 50 iterations) against records produced by the reference
-    deskdft itself (tests/golden/make_golden_level3.py): total energy within 1e-6 Ha (the
+    std(last 5 E) < 1e-9, max 50 iterations) on 32 molecules against records produced by the
+    reference deskdft itself (tests/golden/make_golden_level3.py): total energy within 1e-6 Ha (the
     fp64 bar), gap within 1e-5 eV, same iteration count."""
     import json
     import os
@@ -336,6 +336,7 @@ def test_config5_level3_against_reference(gpu_lib, sto3g):
     g = json.load(open(path))
     mols = [Molecule(tuple(r["Z"]), np.asarray(r["pos_bohr"])) for r in g["molecules"]]
     opts = SCFOptions(**g["options"])
+    assert len(mols) >= 32
     res = scf_batch(mols, sto3g, opts)
     for r, ref in zip(res, g["molecules"]):
         assert abs(r.E_total - ref["E_total"]) < 1e-6, (r.E_total, ref["E_total"])
