@@ -20,7 +20,7 @@
  *   dftb_diis                       <- deskdft.scf.diis_step          (scf.py:101-132)
  *
  * Conventions: all arrays passed in dftb_batch_in / dftb_results are HOST
- * memory; the plan owns every device buffer it allocates (freed by
+ * memory (dftb_results_dev: device memory owned by the caller); the plan owns every device buffer it allocates (freed by
  * dftb_plan_destroy).  Functions taking a `stream` enqueue work on that CUDA
  * stream (cudaStream_t passed as void*; NULL = legacy default stream).
  * Every function returns 0 on success or a DFTB_E* code; dftb_last_error()
@@ -85,7 +85,7 @@ typedef struct {
     int32_t precision;         /* 0 = f64 build, 1 = f32 build (SCFOptions.precision) */
     int32_t max_iterations;    /* >= 5 (scf.py:60-62) */
     double convergence_std;    /* std(last 5 E) threshold; 0 = fixed iteration count */
-    int32_t diis_history;      /* <= 8 */
+    int32_t diis_history;      /* 1..64: DIIS ring slots (the Python layer passes min(diis_history, max_iterations)) */
     int32_t diis_start;
     double damping_factor;
     double screen_eps;         /* Schwarz threshold; primitive cut = 1e-3 * eps */
@@ -120,6 +120,22 @@ int dftb_plan_iterate(dftb_plan *plan, int32_t it, void *stream); /* one SCF ite
 /* Blocks until this plan's last dftb_plan_run has completed (not any later work queued on
  * `stream` by other plans) and copies the results to host memory on the plan's own stream. */
 int dftb_plan_fetch(dftb_plan *plan, dftb_results *out, void *stream);
+/* Results into CALLER-OWNED DEVICE buffers (e.g. PyTorch tensors), same layouts as
+ * dftb_results; NULL members are skipped.  Enqueued on `stream` after this plan's queued
+ * work (stream-ordered; no host synchronisation, the caller's memory is never freed).
+ * Replaces the host copy of scf()'s SCFResult fields (scf.py:202-210) for device consumers. */
+typedef struct {
+    double *E_total;           /* [n_mol] */
+    double *E_comp;            /* [n_mol*5] */
+    double *history;           /* [n_mol*max_iterations], unused tail = NaN */
+    int32_t *iterations;       /* [n_mol] */
+    int32_t *converged;        /* [n_mol] */
+    int32_t *n_mo;             /* [n_mol] */
+    double *epsilon;           /* [n_mol*DFTB_NMAX] */
+    double *C;                 /* [sum_m n_ao(m)^2] */
+    int32_t *status;           /* [n_mol] */
+} dftb_results_dev;
+int dftb_plan_fetch_device(dftb_plan *plan, const dftb_results_dev *out, void *stream);
 int dftb_plan_info(const dftb_plan *plan, int64_t *info, int n_info);  /* sizes, see plan.cu */
 
 /* Operator-level stages (each enqueues device work; results fetched with dftb_plan_get). */

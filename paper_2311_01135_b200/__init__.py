@@ -15,4 +15,4 @@ from .errors import (BasisError, DeskDFTError, DeviceError, DimensionError,  # n
 from .molio import (GeometryManifest, ManifestEntry, Molecule, electron_count, emit_xyz,  # noqa: F401
                     load_manifest, nuclear_repulsion, parse_xyz, save_manifest)
 from .scf import (OrbitalSolution, SCFOptions, SCFResult, diis_step, properties, scf,  # noqa: F401
-                  scf_batch, solve_roothaan)
+                  scf_batch, scf_batch_device, solve_roothaan)

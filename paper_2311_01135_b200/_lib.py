@@ -62,6 +62,11 @@ class Results(ctypes.Structure):
     ]
 
 
+class ResultsDev(ctypes.Structure):
+    """dftb_results_dev: caller-owned DEVICE pointers (same layouts as Results)."""
+    _fields_ = [(name, ctypes.c_void_p) for name, _ in Results._fields_]
+
+
 ST_OVERLAP_NOT_PD, ST_NEG_WEIGHT, ST_XC_NONFINITE, ST_NO_ORBITALS, ST_SINGULAR = 1, 2, 4, 8, 16
 
 _lib = None
@@ -78,6 +83,7 @@ SIGNATURES = {
     "dftb_plan_begin": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
     "dftb_plan_iterate": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p]),
     "dftb_plan_fetch": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Results), ctypes.c_void_p]),
+    "dftb_plan_fetch_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ResultsDev), ctypes.c_void_p]),
     "dftb_plan_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_int]),
     "dftb_plan_one_electron": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
     "dftb_plan_eri": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),

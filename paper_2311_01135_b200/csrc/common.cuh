@@ -19,7 +19,7 @@ constexpr int NPP = NPRIM * NPRIM;   // primitive pairs per shell pair
 constexpr int BOYS_NCOL = 16;        // F_m columns, m = 0..15
 constexpr int BOYS_NT = 431;         // T = 0.0 .. 43.0 step 0.1
 constexpr int PP_FIELDS = 10;        // p, Px, Py, Pz, 1/(2p), c_ss, c_sp, c_ps, c_pp, bound
-constexpr int DIIS_MAX = 8;
+constexpr int DIIS_MAX = 64;   // largest DIIS ring (diis_history, capped by max_iterations on the host)
 constexpr int NCLS = 6;              // quartet classes (LL|LL) (LL|LS) (LL|SS) (LS|LS) (LS|SS) (SS|SS)
 
 HD int64_t tri(int64_t i) { return i * (i + 1) / 2; }
@@ -119,7 +119,7 @@ struct DevBatch {
     double *g_w;              // [n_pts]
     // matrices (each sum nao^2 doubles)
     double *S, *T, *V, *H, *X, *C, *Cp, *rho, *rho_prev, *F, *J, *K, *Vxc, *scratch;
-    double *Fring, *Ering;    // [DIIS_MAX][sum nao^2]
+    double *Fring, *Ering;    // [diis_history][sum nao^2]
     // ERI store (f64 or f32)
     void *eri;
     // partials

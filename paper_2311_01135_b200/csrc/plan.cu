@@ -34,6 +34,7 @@ void launch_orth(const DevBatch &b, int nmax, cudaStream_t s);
 void launch_post(const DevBatch &b, int nmax, int it, int diis_start, int diis_hist, double damping,
                  double conv_std, cudaStream_t s);
 void launch_reduce(const DevBatch &b, int which, cudaStream_t s);
+void launch_fetch_dev(const DevBatch &b, double *E, double *hist, cudaStream_t s);
 void launch_roothaan(const DevBatch &b, int nmax, cudaStream_t s);
 void launch_diis_single(const double *F, const double *E, int mh, int n, double *out, cudaStream_t s);
 void launch_eval_ao(const DevBatch &b, int mol, double *out, cudaStream_t s);
@@ -212,7 +213,7 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
     double tr = trace_ms();
     if (!in || !opts || !out) return fail(DFTB_EINVAL, "null argument");
     if (opts->max_iterations < 1) return fail(DFTB_EINVAL, "max_iterations must be >= 1");
-    if (opts->diis_history < 1 || opts->diis_history > DIIS_MAX) return fail(DFTB_EINVAL, "diis_history must be in 1..8");
+    if (opts->diis_history < 1 || opts->diis_history > DIIS_MAX) return fail(DFTB_EINVAL, "diis_history must be in 1..64");
     cudaStream_t st = (cudaStream_t)stream;
     const int nm = in->n_mol;
     if (nm <= 0) return fail(DFTB_EINVAL, "empty batch");
@@ -508,8 +509,8 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
     size_t o_mats[14];
     for (int k = 0; k < 13; ++k) o_mats[k] = L.add<double>(mat);
     o_mats[13] = L.add<double>(2 * (size_t)mat);                    // scratch: two matrices
-    const size_t o_Fring = L.add<double>((size_t)DIIS_MAX * mat);
-    const size_t o_Ering = L.add<double>((size_t)DIIS_MAX * mat);
+    const size_t o_Fring = L.add<double>((size_t)opts->diis_history * mat);
+    const size_t o_Ering = L.add<double>((size_t)opts->diis_history * mat);
     const size_t o_Gp = L.add<double>(G0[nm]);
     const size_t o_Jp = L.add<double>(Jp0[nm]);
     const size_t o_Vp = L.add<double>(V0[nm]);
@@ -517,7 +518,7 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
     const size_t o_enn = L.add<double>(nm);
     const size_t o_hist = L.add<double>((size_t)nm * maxit);
     const size_t o_comp = L.add<double>(5 * (size_t)nm);
-    const size_t o_Bmat = L.add<double>((size_t)nm * DIIS_MAX * DIIS_MAX);
+    const size_t o_Bmat = L.add<double>((size_t)nm * opts->diis_history * opts->diis_history);
     const size_t o_eps = L.add<double>((size_t)nm * NMAX);
     const size_t o_dbg = L.add<long long>((size_t)nm * 16);
     size_t o_ints[9];
@@ -859,6 +860,28 @@ int dftb_plan_fetch(dftb_plan *p, dftb_results *r, void *stream) {
     return 0;
 }
 
+int dftb_plan_fetch_device(dftb_plan *p, const dftb_results_dev *r, void *stream) {
+    if (!p || !r) return fail(DFTB_EINVAL, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const DevBatch &d = p->d;
+    const int nm = d.n_mol;
+    if (p->fin_rec) CK(cudaStreamWaitEvent(st, p->fin, 0));   // this plan's queued work first
+    const cudaMemcpyKind k = cudaMemcpyDeviceToDevice;
+    if (r->E_total || r->history) launch_fetch_dev(d, r->E_total, r->history, st);
+    if (r->iterations) CK(cudaMemcpyAsync(r->iterations, d.iters, sizeof(int) * nm, k, st));
+    if (r->E_comp) CK(cudaMemcpyAsync(r->E_comp, d.comp, sizeof(double) * 5 * nm, k, st));
+    if (r->converged) CK(cudaMemcpyAsync(r->converged, d.conv, sizeof(int) * nm, k, st));
+    if (r->n_mo) CK(cudaMemcpyAsync(r->n_mo, d.nmo, sizeof(int) * nm, k, st));
+    if (r->epsilon) CK(cudaMemcpyAsync(r->epsilon, d.eps, sizeof(double) * NMAX * nm, k, st));
+    if (r->C) CK(cudaMemcpyAsync(r->C, d.C, sizeof(double) * p->mat0[nm], k, st));
+    if (r->status) CK(cudaMemcpyAsync(r->status, d.status, sizeof(int) * nm, k, st));
+    CK(cudaGetLastError());
+    // the plan's stream-ordered free must also wait for these reads
+    enq_begin(p, st);
+    enq_end(p, st);
+    return 0;
+}
+
 int dftb_scf_batch(const dftb_batch_in *in, const dftb_opts *opts, dftb_results *out, void *stream) {
     dftb_plan *p = nullptr;
     int rc = dftb_plan_create(in, opts, stream, &p);
@@ -1133,7 +1156,7 @@ int dftb_b3lyp(const double *n, const double *sigma, int64_t npts, double *exc, 
 }
 
 int dftb_diis(const double *F, const double *E, int32_t m, int32_t n, double *out, void *stream) {
-    if (m < 1 || m > DIIS_MAX + 1 || n < 1) return fail(DFTB_EINVAL, "diis: need 1 <= m <= 9 entries");
+    if (m < 1 || m > DIIS_MAX || n < 1) return fail(DFTB_EINVAL, "diis: need 1 <= m <= 64 entries");
     cudaStream_t st = (cudaStream_t)stream;
     const size_t nn = (size_t)n * n;
     double *buf = nullptr;

@@ -10,6 +10,7 @@
 //            C = X C' -> rho = 2 C_occ C_occ^T (+ pre-DIIS damping) -> convergence.
 // No host round trip: the host enqueues J/K, XC and post for every iteration.
 #include "common.cuh"
+#include <math_constants.h>
 
 namespace dftb {
 
@@ -25,8 +26,8 @@ struct Arena {
     int *pp, *qq;       // rotation pairs [2][NPH]
     int *perm;          // [NMAX]
     double *dv;         // [NMAX]
-    double *Bs;         // [10*10] DIIS system
-    double *cf;         // [10]
+    double *Bs;         // [hs*hs] DIIS system (hs = history + 1)
+    double *cf;         // [hs]
     double *red;        // [64]
     double *scal;       // [16] scalars broadcast
     long long *dbgp;    // JAC_PHASES builds: [2] angle / apply cycles (else null)
@@ -36,7 +37,8 @@ constexpr int NPH = NMAX / 2 + 1;
 
 HD size_t arena_b(int nm) { return (size_t)(nm * nm > 2 * KP * 64 ? nm * nm : 2 * KP * 64); }
 
-__device__ __forceinline__ Arena carve(unsigned char *base, int nm) {
+// hs: the largest bordered DIIS system (diis_history + 1; 10 for kernels without DIIS)
+__device__ __forceinline__ Arena carve(unsigned char *base, int nm, int hs = 10) {
     Arena a;
     a.nm = nm;
     double *p = (double *)base;
@@ -47,8 +49,8 @@ __device__ __forceinline__ Arena carve(unsigned char *base, int nm) {
     a.cs = p; p += 2 * NPH;
     a.sn = p; p += 2 * NPH;
     a.dv = p; p += NMAX;
-    a.Bs = p; p += 100;
-    a.cf = p; p += 10;
+    a.Bs = p; p += hs * hs;
+    a.cf = p; p += hs;
     a.red = p; p += 64;
     a.scal = p; p += 16;
     a.dbgp = nullptr;
@@ -59,8 +61,8 @@ __device__ __forceinline__ Arena carve(unsigned char *base, int nm) {
     return a;
 }
 
-size_t scf_smem_bytes(int nm) {
-    return sizeof(double) * ((size_t)nm * nm + arena_b(nm) + 4 * NPH + NMAX + 100 + 10 + 64 + 16) +
+size_t scf_smem_bytes(int nm, int hs = 10) {
+    return sizeof(double) * ((size_t)nm * nm + arena_b(nm) + 4 * NPH + NMAX + (size_t)hs * hs + hs + 64 + 16) +
            sizeof(int) * (4 * NPH + NMAX);
 }
 
@@ -304,16 +306,17 @@ __device__ void warp_jacobi_eigs(double *A, int n, const Arena &ar, double tol =
             if (off <= tol * dg || off < 1e-300 || sweeps >= max_sweeps) break;
             ++sweeps;
         }
-        if (lane < np) {
+        for (int kr = lane; kr < np; kr += 32) {
             int p, q;
-            jac_pair(lane, r, n2, p, q);
+            jac_pair(kr, r, n2, p, q);
             double c = 1.0, s1 = 0.0;
             if (q < n) jac_angle(A[p * n + p], A[q * n + q], A[p * n + q], c, s1);
-            ar.cs[lane] = c; ar.sn[lane] = s1; ar.pp[lane] = p; ar.qq[lane] = q;
+            ar.cs[kr] = c; ar.sn[kr] = s1; ar.pp[kr] = p; ar.qq[kr] = q;
         }
         __syncwarp();
-        if (lane < np * np) {
-            const int u = lane / np, v = lane % np;
+        // every 2 x 2 block (u, v) reads and writes only its own four elements
+        for (int uv = lane; uv < np * np; uv += 32) {
+            const int u = uv / np, v = uv % np;
             const double s1 = ar.sn[u], s2 = ar.sn[v], c1 = ar.cs[u], c2 = ar.cs[v];
             const int p1 = ar.pp[u], q1 = ar.qq[u], p2 = ar.pp[v], q2 = ar.qq[v];
             const bool hq1 = q1 < n, hq2 = q2 < n;
@@ -621,6 +624,50 @@ struct PostArgs {
     double damping, conv_std;
 };
 
+// Solve the bordered DIIS system ar.Bs (n1 x n1, rhs e_{n1-1}) -> ar.cf, by one warp:
+// Gaussian elimination with partial pivoting in shared memory (the same operations in the
+// same order per element as a serial elimination; a thread-local array cost a local-memory
+// round trip per element update).  Mx in ar.A (row stride n1 + 1), multipliers in ar.sn.
+__device__ void diis_solve_warp(const Arena &ar, int n1) {
+    const int lane = threadIdx.x & 31;
+    double *Mx = ar.A, *fr = ar.sn;
+    const int W = n1 + 1, nh = n1 - 1;
+    __syncwarp();
+    for (int t = lane; t < n1 * W; t += 32) {
+        const int r = t / W, k = t - r * W;
+        Mx[t] = k < n1 ? ar.Bs[r * n1 + k] : (r == nh ? 1.0 : 0.0);
+    }
+    __syncwarp();
+    for (int c = 0; c < n1; ++c) {
+        int piv = c;
+        for (int r = c + 1; r < n1; ++r)
+            if (fabs(Mx[r * W + c]) > fabs(Mx[piv * W + c])) piv = r;
+        __syncwarp();
+        if (piv != c)
+            for (int k = lane; k <= n1; k += 32) {
+                const double t = Mx[c * W + k];
+                Mx[c * W + k] = Mx[piv * W + k];
+                Mx[piv * W + k] = t;
+            }
+        __syncwarp();
+        for (int r = c + 1 + lane; r < n1; r += 32) fr[r] = Mx[r * W + c] / Mx[c * W + c];
+        __syncwarp();
+        const int wk = n1 + 1 - c;
+        for (int t = lane; t < (n1 - c - 1) * wk; t += 32) {
+            const int r = c + 1 + t / wk, k = c + t % wk;
+            Mx[r * W + k] -= fr[r] * Mx[c * W + k];
+        }
+        __syncwarp();
+    }
+    if (lane == 0)
+        for (int r = n1 - 1; r >= 0; --r) {
+            double s = Mx[r * W + n1];
+            for (int k = r + 1; k < n1; ++k) s -= Mx[r * W + k] * ar.cf[k];
+            ar.cf[r] = s / Mx[r * W + r];
+        }
+    __syncwarp();
+}
+
 __device__ void diis_extrapolate(const DevBatch &b, int m, int N, const double *F, double *Fuse,
                                  const PostArgs &pa, const Arena &ar) {
     const int tid = threadIdx.x;
@@ -633,13 +680,13 @@ __device__ void diis_extrapolate(const DevBatch &b, int m, int N, const double *
         return;
     }
     const int n1 = nh + 1;
-    const double *Bm = b.Bmat + (int64_t)m * DIIS_MAX * DIIS_MAX;
+    const double *Bm = b.Bmat + (int64_t)m * h * h;
     for (int t = tid; t < n1 * n1; t += SCF_THREADS) {
         const int r = t / n1, c = t % n1;
         double v;
         if (r == nh && c == nh) v = 0.0;
         else if (r == nh || c == nh) v = 1.0;
-        else v = Bm[slot(r) * DIIS_MAX + slot(c)];
+        else v = Bm[slot(r) * h + slot(c)];
         ar.Bs[t] = v;
         ar.A[t] = v;
         ar.B[t] = (r == c) ? 1.0 : 0.0;
@@ -662,64 +709,31 @@ __device__ void diis_extrapolate(const DevBatch &b, int m, int N, const double *
             ar.scal[1] = fallback ? 1.0 : 0.0;
         }
         fallback = __shfl_sync(0xffffffffu, fallback, 0);
-        if (!fallback) {
-            // Gaussian elimination with partial pivoting on the bordered system, by the warp in
-            // shared memory (the same operations in the same order per element as a serial
-            // elimination; a thread-local 10 x 11 array cost a local-memory round trip per
-            // element update): Mx in ar.A (row stride W), row multipliers in ar.sn
-            double *Mx = ar.A, *fr = ar.sn;
-            const int W = n1 + 1;
-            __syncwarp();
-            for (int t = lane; t < n1 * W; t += 32) {
-                const int r = t / W, k = t - r * W;
-                Mx[t] = k < n1 ? ar.Bs[r * n1 + k] : (r == nh ? 1.0 : 0.0);
-            }
-            __syncwarp();
-            for (int c = 0; c < n1; ++c) {
-                int piv = c;
-                for (int r = c + 1; r < n1; ++r)
-                    if (fabs(Mx[r * W + c]) > fabs(Mx[piv * W + c])) piv = r;
-                __syncwarp();
-                if (piv != c && lane <= n1) {
-                    const double t = Mx[c * W + lane];
-                    Mx[c * W + lane] = Mx[piv * W + lane];
-                    Mx[piv * W + lane] = t;
-                }
-                __syncwarp();
-                for (int r = c + 1 + lane; r < n1; r += 32) fr[r] = Mx[r * W + c] / Mx[c * W + c];
-                __syncwarp();
-                const int wk = n1 + 1 - c;
-                for (int t = lane; t < (n1 - c - 1) * wk; t += 32) {
-                    const int r = c + 1 + t / wk, k = c + t % wk;
-                    Mx[r * W + k] -= fr[r] * Mx[c * W + k];
-                }
-                __syncwarp();
-            }
-            if (lane == 0)
-                for (int r = n1 - 1; r >= 0; --r) {
-                    double s = Mx[r * W + n1];
-                    for (int k = r + 1; k < n1; ++k) s -= Mx[r * W + k] * ar.cf[k];
-                    ar.cf[r] = s / Mx[r * W + r];
-                }
-        }
+        if (!fallback) diis_solve_warp(ar, n1);
     }
     __syncthreads();
     if (ar.scal[1] != 0.0) {
         const double *Fl = b.Fring + (int64_t)slot(nh - 1) * tot + o;
         const double *Fp = b.Fring + (int64_t)slot(nh - 2) * tot + o;
         for (int t = tid; t < N * N; t += SCF_THREADS) Fuse[t] = 0.5 * Fl[t] + 0.5 * Fp[t];
-    } else {
-        int64_t off[DIIS_MAX];
+    } else if (nh <= 8) {           // the usual history: loads of all entries in flight at once
+        int64_t off[8];
 #pragma unroll
-        for (int a = 0; a < DIIS_MAX; ++a) off[a] = (int64_t)slot(a < nh ? a : 0) * tot + o;
+        for (int a = 0; a < 8; ++a) off[a] = (int64_t)slot(a < nh ? a : 0) * tot + o;
         for (int t = tid; t < N * N; t += SCF_THREADS) {
-            double x[DIIS_MAX];
+            double x[8];
 #pragma unroll
-            for (int a = 0; a < DIIS_MAX; ++a) x[a] = a < nh ? b.Fring[off[a] + t] : 0.0;
+            for (int a = 0; a < 8; ++a) x[a] = a < nh ? b.Fring[off[a] + t] : 0.0;
             double v = 0.0;
 #pragma unroll
-            for (int a = 0; a < DIIS_MAX; ++a)
+            for (int a = 0; a < 8; ++a)
                 if (a < nh) v += ar.cf[a] * x[a];
+            Fuse[t] = v;
+        }
+    } else {
+        for (int t = tid; t < N * N; t += SCF_THREADS) {
+            double v = 0.0;
+            for (int a = 0; a < nh; ++a) v += ar.cf[a] * b.Fring[(int64_t)slot(a) * tot + o + t];
             Fuse[t] = v;
         }
     }
@@ -728,7 +742,7 @@ __device__ void diis_extrapolate(const DevBatch &b, int m, int N, const double *
 
 __global__ void __launch_bounds__(SCF_THREADS, 2) k_post(DevBatch b, PostArgs pa) {
     extern __shared__ __align__(16) unsigned char ssm[];
-    Arena ar = carve(ssm, pa.nm);
+    Arena ar = carve(ssm, pa.nm, pa.diis_hist + 1);
     const int m = b.mol_order[blockIdx.x], tid = threadIdx.x;
     if (b.done[m]) return;
 #ifdef JAC_PHASES
@@ -788,7 +802,7 @@ __global__ void __launch_bounds__(SCF_THREADS, 2) k_post(DevBatch b, PostArgs pa
         __syncthreads();
         // (7) B row for the new entry against every stored error (physical slots)
         const int nh_new = min(b.ring_n[m] + 1, h);
-        double *Bm = b.Bmat + (int64_t)m * DIIS_MAX * DIIS_MAX;
+        double *Bm = b.Bmat + (int64_t)m * h * h;
         for (int a = 0; a < nh_new; ++a) {
             const int sl = (head - a + h) % h;  // walk back from the newest
             const double *Ea = b.Ering + (int64_t)sl * tot + o;
@@ -796,8 +810,8 @@ __global__ void __launch_bounds__(SCF_THREADS, 2) k_post(DevBatch b, PostArgs pa
             for (int t = tid; t < N * N; t += SCF_THREADS) d += Es[t] * Ea[t];
             d = block_sum(d, ar.red);
             if (tid == 0) {
-                Bm[head * DIIS_MAX + sl] = d;
-                Bm[sl * DIIS_MAX + head] = d;
+                Bm[head * h + sl] = d;
+                Bm[sl * h + head] = d;
             }
         }
         __syncthreads();
@@ -907,7 +921,12 @@ __global__ void __launch_bounds__(SCF_THREADS, 2) k_post(DevBatch b, PostArgs pa
     }
 }
 
-static int arena_dim(int nmax) { return nmax < 16 ? 16 : nmax; }
+static int arena_dim(int nmax, int hs = 10) {
+    // the DIIS elimination keeps its hs x (hs + 1) working matrix in A
+    int nm = nmax < 16 ? 16 : nmax;
+    while ((size_t)nm * nm < (size_t)hs * (hs + 1)) ++nm;
+    return nm;
+}
 
 void launch_orth(const DevBatch &b, int nmax, cudaStream_t s) {
     const int nm = arena_dim(nmax);
@@ -918,8 +937,8 @@ void launch_orth(const DevBatch &b, int nmax, cudaStream_t s) {
 
 void launch_post(const DevBatch &b, int nmax, int it, int diis_start, int diis_hist, double damping,
                  double conv_std, cudaStream_t s) {
-    const int nm = arena_dim(nmax);
-    const size_t sm = scf_smem_bytes(nm);
+    const int nm = arena_dim(nmax, diis_hist + 1);
+    const size_t sm = scf_smem_bytes(nm, diis_hist + 1);
     smem_optin((const void *)k_post);
     PostArgs pa{nm, it, diis_start, diis_hist, damping, conv_std};
     k_post<<<b.n_mol, SCF_THREADS, sm, s>>>(b, pa);
@@ -954,12 +973,27 @@ void launch_roothaan(const DevBatch &b, int nmax, cudaStream_t s) {
     k_roothaan<<<b.n_mol, SCF_THREADS, sm, s>>>(b, nm);
 }
 
+// ---------------------------------------------------------------------------- device results
+// E_total[m] = the last recorded energy; history copied with the tail past iters[m] set to NaN
+__global__ void k_fetch(DevBatch b, double *E, double *hist) {
+    const int m = blockIdx.x, nit = b.iters[m];
+    const double *h = b.hist + (int64_t)m * b.max_it;
+    if (E && threadIdx.x == 0) E[m] = nit > 0 ? h[nit - 1] : CUDART_NAN;
+    if (hist)
+        for (int t = threadIdx.x; t < b.max_it; t += blockDim.x)
+            hist[(int64_t)m * b.max_it + t] = t < nit ? h[t] : CUDART_NAN;
+}
+
+void launch_fetch_dev(const DevBatch &b, double *E, double *hist, cudaStream_t s) {
+    k_fetch<<<b.n_mol, 64, 0, s>>>(b, E, hist);
+}
+
 // ---------------------------------------------------------------------------- standalone DIIS
 // One system: F, E given as m x (n x n) arrays; out = diis_step(history) (scf.py:101-132).
 __global__ void __launch_bounds__(SCF_THREADS) k_diis_single(const double *F, const double *E, int mh, int n,
-                                                            double *out) {
+                                                            double *out, int nm) {
     extern __shared__ __align__(16) unsigned char ssm[];
-    const Arena ar = carve(ssm, max(mh + 1, 16));
+    const Arena ar = carve(ssm, nm, mh + 1);
     const int tid = threadIdx.x, nn = n * n;
     if (mh == 1) {
         for (int t = tid; t < nn; t += SCF_THREADS) out[t] = F[t];
@@ -986,32 +1020,16 @@ __global__ void __launch_bounds__(SCF_THREADS) k_diis_single(const double *F, co
     __syncthreads();
     if (tid < 32) warp_jacobi_eigs(ar.A, n1, ar);
     const double *Ad = ar.A;
-    if (tid == 0) {
-        double mx = 0.0, mn = 1e308;
-        for (int i = 0; i < n1; ++i) { const double e = fabs(Ad[i * n1 + i]); mx = fmax(mx, e); mn = fmin(mn, e); }
-        const bool fb = !(mn > 0.0) || (mx / mn > 1e12);
-        ar.scal[1] = fb;
-        if (!fb) {
-            double Mx[10][11];
-            for (int r = 0; r < n1; ++r) {
-                for (int c = 0; c < n1; ++c) Mx[r][c] = ar.Bs[r * n1 + c];
-                Mx[r][n1] = (r == mh) ? 1.0 : 0.0;
-            }
-            for (int c = 0; c < n1; ++c) {
-                int piv = c;
-                for (int r = c + 1; r < n1; ++r) if (fabs(Mx[r][c]) > fabs(Mx[piv][c])) piv = r;
-                if (piv != c) for (int k = 0; k <= n1; ++k) { double t = Mx[c][k]; Mx[c][k] = Mx[piv][k]; Mx[piv][k] = t; }
-                for (int r = c + 1; r < n1; ++r) {
-                    const double f = Mx[r][c] / Mx[c][c];
-                    for (int k = c; k <= n1; ++k) Mx[r][k] -= f * Mx[c][k];
-                }
-            }
-            for (int r = n1 - 1; r >= 0; --r) {
-                double s = Mx[r][n1];
-                for (int k = r + 1; k < n1; ++k) s -= Mx[r][k] * ar.cf[k];
-                ar.cf[r] = s / Mx[r][r];
-            }
+    if (tid < 32) {
+        bool fb = false;
+        if (tid == 0) {
+            double mx = 0.0, mn = 1e308;
+            for (int i = 0; i < n1; ++i) { const double e = fabs(Ad[i * n1 + i]); mx = fmax(mx, e); mn = fmin(mn, e); }
+            fb = !(mn > 0.0) || (mx / mn > 1e12);
+            ar.scal[1] = fb;
         }
+        fb = __shfl_sync(0xffffffffu, fb, 0);
+        if (!fb) diis_solve_warp(ar, n1);
     }
     __syncthreads();
     for (int t = tid; t < nn; t += SCF_THREADS) {
@@ -1023,9 +1041,10 @@ __global__ void __launch_bounds__(SCF_THREADS) k_diis_single(const double *F, co
 }
 
 void launch_diis_single(const double *F, const double *E, int mh, int n, double *out, cudaStream_t s) {
-    const size_t sm = scf_smem_bytes(max(mh + 1, 16));
+    const int nm = arena_dim(mh + 1, mh + 1);
+    const size_t sm = scf_smem_bytes(nm, mh + 1);
     smem_optin((const void *)k_diis_single);
-    k_diis_single<<<1, SCF_THREADS, sm, s>>>(F, E, mh, n, out);
+    k_diis_single<<<1, SCF_THREADS, sm, s>>>(F, E, mh, n, out, nm);
 }
 
 }  // namespace dftb

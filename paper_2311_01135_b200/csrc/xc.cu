@@ -39,6 +39,25 @@ constexpr int XC_THREADS = 256;
 #define XC_MMA 0
 #endif
 constexpr int XC_SHD = 13;       // doubles per shell record in smem
+// f64 part of a shell record in k_xc: centre (x, y, z) and the three exponents in f64
+constexpr int XC_SHD_D = 6;
+// f32 build, AO exponentials.  The reference evaluates phi in f64 and rounds it to f32
+// (xc.py:165-194); XC_AO_EXP=0 (default) forms a r^2 and exp(-a r^2) in f32 (relative error
+// up to ~a r^2 * 2^-24 per primitive).  XC_AO_EXP=1 forms a r^2 in f64 and evaluates
+// exp(-a r^2) = 2^-n exp(-(a r^2 - n ln 2)) with the reduced argument in f32 (~2 ulp of the
+// f64 value).  Measured on B200: V_xc vs the reference's own f32
+// xc_matrix 1.19e-6 -> 1.09e-6 of max|V| at N = 63, configs[1] f32 labels vs the reference
+// f64 MAE 0.150 -> 0.160 meV (max 0.52 -> 0.43) - the f32 contractions dominate - at
+// +0.31 ms (+16%) per XC iteration, so the f32 exponent stays.
+#ifndef XC_AO_EXP
+#define XC_AO_EXP 0
+#endif
+
+__device__ __forceinline__ float expneg_f32acc(double x) {
+    const double n = rint(x * 1.4426950408889634);            // x / ln 2
+    const float f = (float)fma(-n, 0.69314718055994531, x);    // |f| <= 0.35, error ~1e-16 * n
+    return ldexpf(expf(-f), -(int)n);
+}
 
 template <typename W>
 struct Vec4;
@@ -78,7 +97,7 @@ struct XCL {
     static constexpr size_t shd = dw + ((sizeof(W) * 4 * BP + 15) & ~(size_t)15);
     // shell records: centres [nsh][3] f64 (for the point - centre difference), exponents and
     // coefficients [nsh][9] in W (no per-use f64 -> f32 conversions), (ao << 1 | kind) [nsh]
-    static size_t bytes(int nsh) { return shd + (3 * sizeof(double) + 9 * sizeof(W) + sizeof(int)) * (size_t)nsh; }
+    static size_t bytes(int nsh) { return shd + (XC_SHD_D * sizeof(double) + 9 * sizeof(W) + sizeof(int)) * (size_t)nsh; }
 };
 
 template <typename W, int NQ, int BP>
@@ -87,7 +106,7 @@ __device__ __forceinline__ void xc_eval_phi(W *phi, const double *pt, const doub
     constexpr int NP = 4 * NQ, PL = NP * BP;
     for (int t = threadIdx.x; t < BP * nsh; t += XC_THREADS) {
         const int p = t % BP, sh = t / BP;
-        const double *r = shd + 3 * sh;
+        const double *r = shd + XC_SHD_D * sh;
         const W *f = shw + 9 * sh;
         const int kind = shi[sh] & 1, ao = shi[sh] >> 1;
         W v[4][4];  // [plane][component]
@@ -97,8 +116,10 @@ __device__ __forceinline__ void xc_eval_phi(W *phi, const double *pt, const doub
             for (int c = 0; c < 4; ++c) v[a][c] = (W)0;
         if (p < nb) {
             const double *q = pt + 4 * p;
-            const W dx = (W)(q[0] - r[0]), dy = (W)(q[1] - r[1]), dz = (W)(q[2] - r[2]);
-            const W r2 = dx * dx + dy * dy + dz * dz;
+            const double dxd = q[0] - r[0], dyd = q[1] - r[1], dzd = q[2] - r[2];
+            const double r2d = dxd * dxd + dyd * dyd + dzd * dzd;
+            const W dx = (W)dxd, dy = (W)dyd, dz = (W)dzd;
+            const W r2 = (W)r2d;
             constexpr W kCut = sizeof(W) == 4 ? (W)88 : (W)745;
             // unless every primitive underflows (exponents descend, f[2] is the smallest; the
             // AO values and gradients then stay exactly zero, as the loop would give: core
@@ -110,8 +131,16 @@ __device__ __forceinline__ void xc_eval_phi(W *phi, const double *pt, const doub
                 const W a = f[k];
                 const W ar = a * r2;
                 W e;
-                if constexpr (sizeof(W) == 4) e = ar < kCut ? expf(-ar) : (W)0;
-                else e = ar < kCut ? exp(-ar) : (W)0;
+                if constexpr (sizeof(W) == 4) {
+                    if (XC_AO_EXP) {
+                        const double ard = r[3 + k] * r2d;
+                        e = ard < (double)kCut ? expneg_f32acc(ard) : (W)0;
+                    } else {
+                        e = ar < kCut ? expf(-ar) : (W)0;
+                    }
+                } else {
+                    e = ar < kCut ? exp(-ar) : (W)0;
+                }
                 const W m2a = (W)-2 * a;
                 bs += f[3 + k] * e;
                 ds += f[3 + k] * m2a * e;
@@ -164,7 +193,7 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
     double *fpt = (double *)(xsm + L::fpt);
     W *dw = (W *)(xsm + L::dw);
     double *shd = (double *)(xsm + L::shd);
-    W *shw = (W *)(shd + 3 * nsh);
+    W *shw = (W *)(shd + XC_SHD_D * nsh);
     int *shi = (int *)(shw + 9 * nsh);
     const int tid = threadIdx.x;
     const double *rg = b.rho + b.m_mat0[m];
@@ -175,11 +204,12 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
     for (int t = tid; t < 4 * PL; t += XC_THREADS) phi[t] = (W)0;
     for (int sh = tid; sh < nsh; sh += XC_THREADS) {
         const int gsh = s0 + sh;
-        double *r = shd + 3 * sh;
+        double *r = shd + XC_SHD_D * sh;
         W *f = shw + 9 * sh;
         const double *A = b.a_xyz + 3 * b.s_atom[gsh];
         for (int d = 0; d < 3; ++d) {
             r[d] = A[d];
+            r[3 + d] = b.s_exp[3 * gsh + d];
             f[d] = (W)b.s_exp[3 * gsh + d];
             f[3 + d] = (W)b.s_cs[3 * gsh + d];
             f[6 + d] = (W)b.s_cp[3 * gsh + d];

@@ -179,6 +179,13 @@ class Plan:
             return out.reshape(n, n)
         return out
 
+    def fetch_device(self, out: dict):
+        """Enqueue the results into caller-owned device tensors (torch, on this plan's device)
+        on the plan's stream; no host synchronisation.  Keys: the dftb_results_dev members."""
+        ptrs = {k: ctypes.c_void_p(int(v.data_ptr())) for k, v in out.items()}
+        r = _lib.ResultsDev(**ptrs)
+        _lib.check(self.lib.dftb_plan_fetch_device(self.h, ctypes.byref(r), self.stream))
+
     def fetch(self, want_C: bool = True) -> BatchResults:
         pk = self.pk
         nm, mi = pk.n_mol, int(self.opts.max_iterations)

@@ -15,6 +15,7 @@ f32 (the reference's f32 BLAS path), everything else in f64.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -23,13 +24,14 @@ from . import _lib
 from .basis import BasisSet, expand
 from .constants import HARTREE_TO_EV
 from .engine import EngineOptions, Plan, status_error
-from .errors import DeskDFTError, DimensionError, MoleculeError
+from .errors import DeskDFTError, DimensionError, MoleculeError, ResourceLimitError
 from .grids import check_level
 from .molio import Molecule, electron_count
 
 EXACT_EXCHANGE_FRACTION = 0.20
 LINDEP_THRESHOLD = 1e-7
 DIIS_COND_MAX = 1e12
+DIIS_RING_MAX = 64        # device DIIS ring (csrc/common.cuh DIIS_MAX)
 
 
 @dataclass(frozen=True)
@@ -66,17 +68,28 @@ class SCFOptions:
             raise DeskDFTError("max_iterations must be >= 5 (convergence window needs 5 energies)")
         if self.precision not in ("f32", "f64"):
             raise DeskDFTError(f"precision must be 'f32' or 'f64', got {self.precision!r}")
-        if not 1 <= self.diis_history <= 8:
-            raise DeskDFTError("diis_history must be between 1 and 8 on the device path")
 
     @property
     def dtype(self):
         return np.float32 if self.precision == "f32" else np.float64
 
+    def ring(self) -> int:
+        """DIIS ring slots: the reference keeps the last diis_history (F, error) pairs, so
+        never more than max_iterations of them (scf.py:191-195).  diis_history <= 0 leaves
+        the buffer empty, which the reference's diis_step rejects once DIIS is reached."""
+        h = min(int(self.diis_history), int(self.max_iterations))
+        if h < 1:
+            if self.diis_start <= self.max_iterations:
+                raise DeskDFTError("diis_step requires at least one (F, error) pair")
+            return 1                      # DIIS never runs
+        if h > DIIS_RING_MAX:
+            raise ResourceLimitError(f"diis_history={h} exceeds the device DIIS ring ({DIIS_RING_MAX})")
+        return h
+
     def engine(self) -> EngineOptions:
         check_level(self.grid_level)
         return EngineOptions(self.precision, self.max_iterations, self.convergence_std,
-                             self.diis_history, self.diis_start, self.damping_factor,
+                             self.ring(), self.diis_start, self.damping_factor,
                              self.screen_eps, self.grid_level)
 
 
@@ -106,6 +119,60 @@ def scf_batch(mols: list[Molecule], b: BasisSet, opts: SCFOptions | None = None,
     if not mols:
         return []
     return finish_batch(start_batch(mols, b, opts, stream), opts, errors)
+
+
+class DeviceLabels(dict):
+    """The tensors of scf_batch_device, plus the device plan they were computed by: the
+    plan is released (stream-ordered) by close() / garbage collection, so the call itself
+    never waits for the device."""
+
+    def __init__(self, tensors: dict, plan: Plan):
+        super().__init__(tensors)
+        self._plan = plan
+
+    def close(self):
+        if self._plan is not None:
+            self._plan.close()
+            self._plan = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def scf_batch_device(mols: list[Molecule], b: BasisSet, opts: SCFOptions | None = None,
+                     with_orbitals: bool = False) -> DeviceLabels:
+    """scf_batch for device consumers: the labels land in torch tensors on the current CUDA
+    device, written on the current torch stream with no host synchronisation (the caller
+    owns the tensors; dftb_plan_fetch_device).  Keys: E_total [n] f64, E_comp [n, 5],
+    history [n, max_iterations] (NaN past `iterations`), iterations / converged / n_mo /
+    status [n] i32, epsilon [n, NMAX] (ascending, first n_mo valid) and, with
+    with_orbitals, C (concatenated row-major n_ao x n_ao blocks).  Per-molecule failures
+    are reported through `status` (DFTB_ST_* bits), not raised."""
+    import torch
+
+    opts = opts or SCFOptions()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    plan = start_batch(mols, b, opts, stream)
+    try:
+        n, mi = int(plan.pk.n_mol), int(opts.max_iterations)
+        f64 = dict(dtype=torch.float64, device=dev)
+        i32 = dict(dtype=torch.int32, device=dev)
+        out = {"E_total": torch.empty(n, **f64), "E_comp": torch.empty((n, 5), **f64),
+               "history": torch.empty((n, mi), **f64), "iterations": torch.empty(n, **i32),
+               "converged": torch.empty(n, **i32), "n_mo": torch.empty(n, **i32),
+               "epsilon": torch.empty((n, _lib.NMAX), **f64), "status": torch.empty(n, **i32)}
+        if with_orbitals:
+            nao = np.asarray(plan.pk.mol_nao, dtype=np.int64)
+            out["C"] = torch.empty(int((nao * nao).sum()), **f64)
+        plan.fetch_device(out)
+    except BaseException:
+        plan.close()
+        raise
+    return DeviceLabels(out, plan)
 
 
 def start_batch(mols: list[Molecule], b: BasisSet, opts: SCFOptions, stream=None) -> Plan:
@@ -222,6 +289,8 @@ def diis_step(history: list) -> np.ndarray:
         raise DeskDFTError("diis_step requires at least one (F, error) pair")
     if len(history) == 1:
         return history[0][0]
+    if len(history) > DIIS_RING_MAX:
+        raise ResourceLimitError(f"{len(history)} DIIS entries exceed the device limit {DIIS_RING_MAX}")
     lib = _lib.load()
     F = np.ascontiguousarray(np.stack([h[0] for h in history]), dtype=np.float64)
     E = np.ascontiguousarray(np.stack([h[1] for h in history]), dtype=np.float64)

@@ -229,6 +229,37 @@ def test_grid_ao_xc(gpu_lib, sto3g, golden, golden_arrays, name):
         np.testing.assert_allclose(x.V_xc, golden_arrays[f"{name}_vxc{lvl}"], rtol=0, atol=1e-10)
 
 
+F32_CASES = [(n, "small", f"{n}_rho", f"{n}_J32", f"{n}_K32", f"{n}_vxc0_f32", "exc0_f32")
+             for n in ("h2", "h2o", "nh3", "ch4", "hf", "dh2o")] + \
+            [("syneri", "synth_eri", "syneri_rho", "syneri_J32", "syneri_K32", "syneri_vxc0_32", "exc0_32")]
+
+
+@pytest.mark.parametrize("case", F32_CASES, ids=[c[0] for c in F32_CASES])
+def test_f32_operators_vs_reference_f32(gpu_lib, sto3g, golden, golden_arrays, case):
+    """The f32 working-dtype operators against the reference's own f32 outputs (reference
+    integrals.py:199-218 over eri_packed(dtype=float32) with f32 rho; xc.py:320-350 over
+    eval_ao(dtype=float32) at grid level 0).  Bounds are ~2.5x the measured maxima relative to
+    the matrix scale (J 4.7e-7, K 6.4e-7, V_xc 1.2e-6; E_xc 2.6e-6 Ha at N = 63): the device
+    forms the f32 products in FP32 (J/K partial sums of 4 products, the reference multiplies in
+    f64) and evaluates the AO exponentials in f32."""
+    name, grp, kr, kj, kk, kv, ke = case
+    rec = golden[grp] if grp == "synth_eri" else golden[grp][name]
+    m = _mol(rec)
+    ao = expand(m, sto3g)
+    g = golden_arrays
+    rho32 = g[kr].astype(np.float32)
+    J, K = G_int.build_jk(G_int.eri_packed(ao, screen_eps=0.0, dtype=np.float32), rho32)
+    assert J.dtype == np.float32 and K.dtype == np.float32
+    rel = lambda u, v: np.abs(u.astype(np.float64) - v.astype(np.float64)).max() / np.abs(v).max()
+    assert rel(J, g[kj]) < 1.5e-6
+    assert rel(K, g[kk]) < 1.5e-6
+    gr = G_xc.build_grid(m, 0)
+    x = G_xc.xc_matrix(gr, G_xc.eval_ao(ao, gr, dtype=np.float32), rho32)
+    assert x.V_xc.dtype == np.float32
+    assert rel(x.V_xc, g[kv]) < 3e-6
+    assert abs(x.E_xc - rec[ke]) < 6e-6
+
+
 def test_b3lyp_device(gpu_lib, golden_arrays):
     g = golden_arrays
     e, vr, vs = G_xc.b3lyp(g["b3lyp_n"], g["b3lyp_s"])
@@ -236,6 +267,36 @@ def test_b3lyp_device(gpu_lib, golden_arrays):
         np.testing.assert_allclose(a, b, rtol=1e-10, atol=0)
     e32, _, _ = G_xc.b3lyp(g["b3lyp_n"].astype(np.float32), g["b3lyp_s"].astype(np.float32))
     assert e32.dtype == np.float32 and np.isfinite(e32).all()
+
+
+@pytest.mark.parametrize("hist", [2, 12, 25])
+def test_diis_history_sizes_vs_oracle(gpu_lib, sto3g, oracle, hist):
+    """diis_history other than the default 8, including rings longer than 8 (the reference
+    imposes no limit, scf.py:46-62,191-195): device SCF vs the oracle's driver."""
+    m = synth.batch(1, 4, seed=21)[0]
+    r = scf(m, sto3g, SCFOptions(diis_history=hist, max_iterations=25, convergence_std=0.0, grid_level=0))
+    ref = oracle.scf(oracle.Mol(m.atomic_numbers, m.positions), "f64", 25, 0.0, 0, diis_history=hist)
+    np.testing.assert_allclose(r.energy_history, ref.history, rtol=0, atol=1e-8)
+    assert abs(r.E_total - ref.E_total) < 1e-9
+
+
+def test_diis_device_long_history(gpu_lib):
+    """The standalone diis_step with 20 entries against the reference algorithm (numpy)."""
+    rng = np.random.default_rng(7)
+    n, k = 12, 20
+    F = [(lambda a: a + a.T)(rng.standard_normal((n, n))) for _ in range(k)]
+    E = [(lambda a: a - a.T)(rng.standard_normal((n, n))) * 0.1 for _ in range(k)]
+    out = diis_step(list(zip(F, E)))
+    B = np.ones((k + 1, k + 1))
+    B[-1, -1] = 0.0
+    for a in range(k):
+        for c in range(k):
+            B[a, c] = float(E[a].ravel() @ E[c].ravel())
+    rhs = np.zeros(k + 1)
+    rhs[-1] = 1.0
+    assert np.linalg.cond(B) < 1e12
+    cf = np.linalg.solve(B, rhs)[:k]
+    np.testing.assert_allclose(out, sum(c * f for c, f in zip(cf, F)), atol=1e-10)
 
 
 def test_diis_device(gpu_lib, golden_arrays):

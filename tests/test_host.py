@@ -131,3 +131,19 @@ def test_batch_pack_layout(sto3g):
     assert int(pk.mol_npts.sum()) == int(pk.atom_tmpln.sum())
     with pytest.raises(MoleculeError):
         batch.pack([parse_xyz("2\ncharge=-4\nH 0 0 0\nH 0 0 1.4", unit="bohr")], sto3g, 0)
+
+
+def test_diis_ring_sizing():
+    """DIIS ring slots follow the reference's buffer (scf.py:191-195: keep the last
+    diis_history pairs, so at most max_iterations of them); an empty buffer is the
+    reference's diis_step error once DIIS is reached."""
+    from paper_2311_01135_b200 import DeskDFTError, ResourceLimitError, SCFOptions
+
+    assert SCFOptions().engine().diis_history == 8
+    assert SCFOptions(diis_history=20, max_iterations=12).engine().diis_history == 12
+    assert SCFOptions(diis_history=40, max_iterations=50).engine().diis_history == 40
+    with pytest.raises(DeskDFTError, match="at least one"):
+        SCFOptions(diis_history=0, max_iterations=10).engine()
+    assert SCFOptions(diis_history=0, max_iterations=10, diis_start=11).engine().diis_history == 1
+    with pytest.raises(ResourceLimitError):
+        SCFOptions(diis_history=100, max_iterations=100).engine()

@@ -79,3 +79,33 @@ def test_mixed_size_batches_in_flight(gpu_lib):
     for k in (1, 2):
         ref = [r.E_total for r in scf_batch(batches[k], b, opts)]
         assert [r.E_total for r in got[k]] == ref
+
+
+def test_scf_batch_device_outputs(gpu_lib):
+    """dftb_plan_fetch_device: labels written into caller-owned torch tensors on the current
+    stream equal the host results of scf_batch bit for bit."""
+    import torch
+
+    from paper_2311_01135_b200 import scf_batch_device, synth
+
+    b = load_basis("sto-3g")
+    mols = synth.batch(5, 3, seed=77)
+    opts = SCFOptions(max_iterations=8, convergence_std=0.0, grid_level=0, precision="f32")
+    ref = scf_batch(mols, b, opts)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        out = scf_batch_device(mols, b, opts, with_orbitals=True)
+        e_host = out["E_total"].cpu()          # ordered on the same stream
+    s.synchronize()
+    assert out["E_total"].is_cuda and out["E_total"].dtype == torch.float64
+    for m, r in enumerate(ref):
+        assert e_host[m].item() == r.E_total
+        n = int(out["iterations"][m])
+        assert n == r.iterations
+        assert out["history"][m, :n].cpu().tolist() == r.energy_history
+        assert torch.isnan(out["history"][m, n:]).all()
+        nmo = int(out["n_mo"][m])
+        assert out["epsilon"][m, :nmo].cpu().numpy().astype(r.solution.epsilon.dtype).tolist() == \
+            r.solution.epsilon.tolist()
+        assert int(out["status"][m]) == 0
+    out.close()
