@@ -146,17 +146,25 @@ struct KetSmem {
     }
 };
 
-// One thread = one screened shell quartet x one ket-component slice (blockIdx.y).
-// KPS: ket components per slice (0 = all): a slice recomputes the Boys function and
+// One thread = one screened shell quartet x one component slice (blockIdx.y).
+// KPS: inner-pair components per slice (0 = all): a slice recomputes the Boys function and
 // R_tuv of all 81 primitive quartets, so fewer slices trade registers for less recomputation.
-// KSM: keep the ket records in shared memory (off for SS|SS, whose occupancy it would cut
-// from 9 to 3 CTAs per SM for a class that is cheap per primitive quartet)
+// SW (swapped roles): lanes of a warp hold consecutive quartets of one bra pair P and
+// consecutive ket pairs Q, so P's primitive records are warp-uniform and Q's per-lane.  The
+// McMurchie-Davidson loop reads its inner pair's records 81 times per quartet and its outer
+// pair's 9 times; with SW the per-lane ket pair is the outer one and the warp-uniform bra pair
+// the inner one (broadcast loads from L1), i.e. (ab|cd) is evaluated as (cd|ab) and the
+// slices run over bra components.  Without SW the ket records are re-read per bra primitive
+// and KSM keeps them in shared memory.
 template <int KA, int KB, int KC, int KD, int KPS, typename ST, bool KSM = true, int MINB = 1,
-          int NS = ((KC || KD) ? 7 : 6)>
+          int NS = ((KC || KD) ? 7 : 6), bool SW = false>
 __global__ void __launch_bounds__(ERI_T, MINB) k_eri(DevBatch b, int cls, double eps, double prim_cut, ST *eri) {
     constexpr int NA = KA ? 4 : 1, NB = KB ? 4 : 1, NC = KC ? 4 : 1, ND = KD ? 4 : 1;
-    constexpr int NKET = NC * ND, NKS = KPS ? KPS : NKET, NSL = NKET / NKS;
-    static_assert(NKET % NKS == 0, "slice size must divide the ket component count");
+    constexpr int NOUT = SW ? NC * ND : NA * NB;              // outer-pair components
+    constexpr int NIN = SW ? NA * NB : NC * ND;               // inner-pair components (sliced)
+    constexpr int NKS = KPS ? KPS : NIN, NSL = NIN / NKS;
+    static_assert(NIN % NKS == 0, "slice size must divide the inner component count");
+    static_assert(!(SW && KSM), "the swapped form reads its inner (bra) records by broadcast");
     const int64_t *pre = b.cls0 + (int64_t)cls * (b.n_mol + 1);
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= pre[b.n_mol]) return;
@@ -186,12 +194,14 @@ __global__ void __launch_bounds__(ERI_T, MINB) k_eri(DevBatch b, int cls, double
     const int64_t base = b.m_eri0[m];
     static_switch<NSL>(blockIdx.y, [&](auto slc) {
         constexpr int KC0 = decltype(slc)::value * NKS;
-        double out[NA * NB][NKS];
+        double out[NOUT][NKS];
 #pragma unroll
-        for (int x = 0; x < NA * NB; ++x)
+        for (int x = 0; x < NOUT; ++x)
 #pragma unroll
             for (int y = 0; y < NKS; ++y) out[x][y] = 0.0;
-        if constexpr (KSM) {
+        if constexpr (SW) {
+            eri_quartet_kv<KC, KD, KA, KB, KC0, NKS>(V, V, Qp, Pp, C, D, A, B, b.boys, prim_cut, out);
+        } else if constexpr (KSM) {
             const KS VK{eri_ksm, (int)threadIdx.x, V};
             eri_quartet_kv<KA, KB, KC, KD, KC0, NKS>(V, VK, Pp, Qp, A, B, C, D, b.boys, prim_cut, out);
         } else {
@@ -201,11 +211,12 @@ __global__ void __launch_bounds__(ERI_T, MINB) k_eri(DevBatch b, int cls, double
         // (i >= j) component writes, for a diagonal quartet only the (ij >= kl) image
         const bool dab = b.p_sa[Pp] == b.p_sb[Pp], dcd = b.p_sa[Qp] == b.p_sb[Qp], dpq = Pp == Qp;
 #pragma unroll
-        for (int x = 0; x < NA * NB; ++x)
+        for (int x = 0; x < NOUT; ++x)
 #pragma unroll
             for (int y = 0; y < NKS; ++y) {
-                const int kc = KC0 + y;
-                const int i = ia + x / NB, j = ib + x % NB, k = ic + kc / ND, l = id + kc % ND;
+                const int xi = SW ? KC0 + y : x;          // bra component index (a, b)
+                const int yk = SW ? x : KC0 + y;          // ket component index (c, d)
+                const int i = ia + xi / NB, j = ib + xi % NB, k = ic + yk / ND, l = id + yk % ND;
                 if (dab && i < j) continue;
                 if (dcd && k < l) continue;
                 if (dpq && pidx(i, j) < pidx(k, l)) continue;
@@ -286,13 +297,14 @@ void launch_schwarz(const DevBatch &b, const int64_t *host_totals, cudaStream_t 
 }
 
 template <int KA, int KB, int KC, int KD, int KPS, bool KSM = true, int MINB = 1, int NS = ((KC || KD) ? 7 : 6),
-          typename ST>
+          bool SW = false, typename ST>
 static void launch_cls(const DevBatch &b, int cls, int64_t n, double eps, double prim_cut, ST *eri,
                        cudaStream_t s, int *nlaunch) {
     if (!n) return;
-    constexpr int NKET = (KC ? 4 : 1) * (KD ? 4 : 1), NSL = NKET / (KPS ? KPS : NKET);
+    constexpr int NIN = SW ? (KA ? 4 : 1) * (KB ? 4 : 1) : (KC ? 4 : 1) * (KD ? 4 : 1);
+    constexpr int NSL = NIN / (KPS ? KPS : NIN);
     const size_t sm = KSM ? sizeof(double) * KetSmem<(KC || KD), NS>::NSLOT * 9 * ERI_T : 0;
-    auto kern = k_eri<KA, KB, KC, KD, KPS, ST, KSM, MINB, NS>;
+    auto kern = k_eri<KA, KB, KC, KD, KPS, ST, KSM, MINB, NS, SW>;
     smem_optin((const void *)kern);
     kern<<<dim3(nblk(n, ERI_T), NSL), ERI_T, sm, s>>>(b, cls, eps, prim_cut, eri);
     ++*nlaunch;
@@ -336,7 +348,7 @@ static void launch_cls(const DevBatch &b, int cls, int64_t n, double eps, double
 #define ERI_LSSS_KSM false     // LS|SS: no ket cache, 8 CTAs/SM (64 registers): 13.0 -> 12.2 ms
 #endif
 #ifndef ERI_LSSS_MINB
-#define ERI_LSSS_MINB 8
+#define ERI_LSSS_MINB 6     // swapped LS|SS: 6 CTAs/SM (85 registers, no spills): 11.84 -> 11.61 ms
 #endif
 #ifndef ERI_SSSS_MINB
 #define ERI_SSSS_MINB 12      // SS|SS: 12 CTAs/SM by registers (40): 5.61 -> 5.10 ms
@@ -348,15 +360,32 @@ static void launch_cls(const DevBatch &b, int cls, int64_t n, double eps, double
 #define ERI_KPS_LS 2       // LL|LS: 2 slices of 2
 #endif
 
+// Swapped roles (SW, see k_eri) per class, measured per class on B200 (ncu, 256 x 9-heavy
+// batch, ms): LS|LS 7.33 -> 7.14, LS|SS 12.13 -> 11.83, SS|SS 5.01 -> 4.56; LL|LL 5.28 -> 5.44,
+// LL|SS 4.09 -> 4.88 and LL|LS 9.60 -> 16.4 (the bra-component slices recompute R_tuv) stay
+// unswapped.
+#ifndef ERI_SW_LSLS
+#define ERI_SW_LSLS 1
+#endif
+#ifndef ERI_SW_LSSS
+#define ERI_SW_LSSS 1
+#endif
+#ifndef ERI_SW_SSSS
+#define ERI_SW_SSSS 1
+#endif
+
 template <typename ST>
 static void launch_eri_t(const DevBatch &b, const int64_t *tot, double eps, double prim_cut,
                          ST *eri, cudaStream_t s, int *nlaunch) {
     launch_cls<1, 1, 1, 1, ERI_KPS_LL, true, ERI_LLLL_MINB, ERI_LLLL_NS>(b, 0, tot[0], eps, prim_cut, eri, s, nlaunch);
     launch_cls<1, 1, 1, 0, ERI_KPS_LS, true, ERI_LLLS_MINB, ERI_LLLS_NS>(b, 1, tot[1], eps, prim_cut, eri, s, nlaunch);
     launch_cls<1, 1, 0, 0, 0, ERI_LLSS_KSM, ERI_LLSS_MINB>(b, 2, tot[2], eps, prim_cut, eri, s, nlaunch);
-    launch_cls<1, 0, 1, 0, 0, ERI_LSLS_KSM, ERI_LSLS_MINB, ERI_LSLS_NS>(b, 3, tot[3], eps, prim_cut, eri, s, nlaunch);
-    launch_cls<1, 0, 0, 0, 0, ERI_LSSS_KSM, ERI_LSSS_MINB>(b, 4, tot[4], eps, prim_cut, eri, s, nlaunch);
-    launch_cls<0, 0, 0, 0, 0, false, ERI_SSSS_MINB>(b, 5, tot[5], eps, prim_cut, eri, s, nlaunch);
+    if (ERI_SW_LSLS) launch_cls<1, 0, 1, 0, 0, false, ERI_LSLS_MINB, 7, true>(b, 3, tot[3], eps, prim_cut, eri, s, nlaunch);
+    else launch_cls<1, 0, 1, 0, 0, ERI_LSLS_KSM, ERI_LSLS_MINB, ERI_LSLS_NS>(b, 3, tot[3], eps, prim_cut, eri, s, nlaunch);
+    if (ERI_SW_LSSS) launch_cls<1, 0, 0, 0, 0, false, ERI_LSSS_MINB, 6, true>(b, 4, tot[4], eps, prim_cut, eri, s, nlaunch);
+    else launch_cls<1, 0, 0, 0, 0, ERI_LSSS_KSM, ERI_LSSS_MINB>(b, 4, tot[4], eps, prim_cut, eri, s, nlaunch);
+    if (ERI_SW_SSSS) launch_cls<0, 0, 0, 0, 0, false, ERI_SSSS_MINB, 6, true>(b, 5, tot[5], eps, prim_cut, eri, s, nlaunch);
+    else launch_cls<0, 0, 0, 0, 0, false, ERI_SSSS_MINB>(b, 5, tot[5], eps, prim_cut, eri, s, nlaunch);
 }
 
 void launch_eri(const DevBatch &b, const int64_t *tot, double eps, double prim_cut, cudaStream_t s,

@@ -233,9 +233,20 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
     int bad = 0;
     const int pg = tid / LG, lg = tid % LG;
     const int64_t p0 = b.xc_p0[cta], p1 = b.xc_p1[cta];
+#ifdef XC_PHASES
+    long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tck = clock64();
+    int nsub = 0;
+#define XP(k) do { const long long t_ = clock64(); ph[k] += t_ - tck; tck = t_; } while (0)
+#else
+#define XP(k) do { } while (0)
+#endif
     for (int64_t sb = p0; sb < p1; sb += BP) {
         const int nb = (int)min((int64_t)BP, p1 - sb);
+#ifdef XC_PHASES
+        ++nsub;
+#endif
         __syncthreads();                                   // previous sub-block consumed
+        XP(5);
         if (tid < BP) {
             const int64_t gi = sb + min(tid, nb - 1);
             pt[4 * tid] = b.g_xyz[3 * gi];
@@ -244,8 +255,10 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
             pt[4 * tid + 3] = tid < nb ? b.g_w[gi] : 0.0;
         }
         __syncthreads();
+        XP(0);
         xc_eval_phi<W, NQ, BP>(phi, pt, shd, shw, shi, nsh, nb);
         __syncthreads();
+        XP(1);
         {   // ---- t = phi^T rho for 4 points x 4 AOs, then n and grad n partials
             W n4[4] = {0, 0, 0, 0}, g4[3][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}};
 #pragma unroll
@@ -367,6 +380,7 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
                 }
         }
         __syncthreads();
+        XP(2);
         if (tid < 3 * BP) {   // ---- functional (f64): parts on three thread groups, one point each
             const int pt_i = tid % BP, part = tid / BP;
             const double *dq = dn + 4 * pt_i;
@@ -411,6 +425,7 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
             }
         }
         __syncthreads();
+        XP(3);
         {   // ---- wv = a phi + b . grad phi; this thread's point is fixed (XC_THREADS % BP == 0)
             static_assert(XC_THREADS % BP == 0, "fixed point per thread");
             const int p = tid % BP;
@@ -421,6 +436,7 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
             }
         }
         __syncthreads();
+        XP(4);
 #pragma unroll
         for (int j = 0; j < TJ; ++j) {                     // ---- V += phi wv^T, 4 x 4 tiles
             const int T = tid + j * XC_THREADS;
@@ -453,6 +469,12 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
             }
         }
     }
+#ifdef XC_PHASES
+    if (blockIdx.x % 97 == 0 && tid == 0)
+        printf("xcffma NQ %d cta %d sub %d: pts %lld phi %lld t %lld func %lld wv %lld V+loop %lld\n", NQ,
+               blockIdx.x, nsub, ph[0], ph[1], ph[2], ph[3], ph[4], ph[5]);
+#endif
+#undef XP
     const int local = cta - b.m_xccta0[m];
     double *Vp = b.Vpart + b.m_V0[m] + (int64_t)local * N * N;
 #pragma unroll
