@@ -348,7 +348,7 @@ static void launch_cls(const DevBatch &b, int cls, int64_t n, double eps, double
 #define ERI_LSSS_KSM false     // LS|SS: no ket cache, 8 CTAs/SM (64 registers): 13.0 -> 12.2 ms
 #endif
 #ifndef ERI_LSSS_MINB
-#define ERI_LSSS_MINB 6     // swapped LS|SS: 6 CTAs/SM (85 registers, no spills): 11.84 -> 11.61 ms
+#define ERI_LSSS_MINB 8
 #endif
 #ifndef ERI_SSSS_MINB
 #define ERI_SSSS_MINB 12      // SS|SS: 12 CTAs/SM by registers (40): 5.61 -> 5.10 ms
@@ -360,18 +360,20 @@ static void launch_cls(const DevBatch &b, int cls, int64_t n, double eps, double
 #define ERI_KPS_LS 2       // LL|LS: 2 slices of 2
 #endif
 
-// Swapped roles (SW, see k_eri) per class, measured per class on B200 (ncu, 256 x 9-heavy
-// batch, ms): LS|LS 7.33 -> 7.14, LS|SS 12.13 -> 11.83, SS|SS 5.01 -> 4.56; LL|LL 5.28 -> 5.44,
-// LL|SS 4.09 -> 4.88 and LL|LS 9.60 -> 16.4 (the bra-component slices recompute R_tuv) stay
-// unswapped.
+// Swapped roles (SW, see k_eri) per class, measured per class on B200 (ncu, kernels alone,
+// 256 x 9-heavy batch, ms): LS|LS 7.33 -> 7.14, LS|SS 12.13 -> 11.61 (6 CTAs/SM), SS|SS 5.01 ->
+// 4.56; LL|LL 5.28 -> 5.44, LL|SS 4.09 -> 4.88, LL|LS 9.60 -> 16.4 (the bra-component slices
+// recompute R_tuv).  In the pipelined stage (one-electron / grid kernels on the aux stream, three
+// batches in flight) the swapped S classes made the stage slower, 47.7 -> 49.5 ms, and the
+// bench 2127 -> 2088 mol/s (same-box A/B), so every class runs unswapped by default.
 #ifndef ERI_SW_LSLS
-#define ERI_SW_LSLS 1
+#define ERI_SW_LSLS 0
 #endif
 #ifndef ERI_SW_LSSS
-#define ERI_SW_LSSS 1
+#define ERI_SW_LSSS 0
 #endif
 #ifndef ERI_SW_SSSS
-#define ERI_SW_SSSS 1
+#define ERI_SW_SSSS 0
 #endif
 
 template <typename ST>
