@@ -237,15 +237,38 @@ def _hbm_peak():
         return 7700.0, "B200_PROFILING.md fallback (HBM3e nominal)"
 
 
-def _eri_traffic():
-    """DRAM bytes (read + write) of one step's ERI stage from the committed ncu --set full
-    capture (profiles/r1_eri_traffic.json), or None when the summary is absent."""
+def _ncu_capture():
+    """The newest committed ncu --set full summary (profiles/*_ncu_full_metrics.json, written by
+    tools/prof_r2.sh) whose build hash is the md5 of the library this process runs, else
+    (None, reason): traffic figures are only quoted from a capture of the same build."""
+    import glob
+    import hashlib
+
+    lib = os.path.join(ROOT, "paper_2311_01135_b200", "libqm1b_b200.so")
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_eri_traffic.json")) as fh:
-            d = json.load(fh)
-        return d["eri_stage_dram_read_bytes"] + d["eri_stage_dram_write_bytes"]
-    except (OSError, KeyError, ValueError):
-        return None
+        h = hashlib.md5(open(lib, "rb").read()).hexdigest()
+    except OSError:
+        return None, "library missing"
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_full_metrics.json")), reverse=True):
+        try:
+            with open(f) as fh:
+                d = json.load(fh)
+        except (OSError, ValueError):
+            continue
+        if d.get("_build") == h:
+            return d, os.path.relpath(f, ROOT)
+    return None, f"no committed ncu capture of this build (md5 {h[:12]})"
+
+
+def _dram_bytes(entries):
+    """Sum of dram__bytes_read.sum + dram__bytes_write.sum over ncu summary entries (bytes)."""
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    tot = 0.0
+    for e in entries:
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            v, u = e[k].split()
+            tot += float(v) * scale[u]
+    return tot
 
 
 def run_ours(args, ws, rank, local):
@@ -328,6 +351,7 @@ def run_ours(args, ws, rank, local):
     achieved_iso = flops / (iso_stage[0] / 1000.0) / 1e12
     # ---------------- XC and J/K kernels against their own rooflines (re-run on the resident density)
     ms_jk, ms_xc = plan.kernel_times(5)
+    ms_post = plan.post_time(5)          # advances the plan's SCF state: after the fetch above
     nao = np.asarray(plan.pk.mol_nao, dtype=np.float64)
     npts = np.asarray(plan.pk.mol_npts, dtype=np.float64)
     xc_flops = float(np.sum(4.0 * nao * nao * npts))            # two N^2 contractions per grid point
@@ -336,6 +360,19 @@ def run_ours(args, ws, rank, local):
     xc_tf = xc_flops / (ms_xc / 1000.0) / 1e12
     jk_gbs = info["eri_bytes"] / (ms_jk / 1000.0) / 1e9
     hbm_peak, hbm_src = _hbm_peak()
+    post_flops = float(np.sum(23.0 * nao ** 3))                   # 9 N^3 + 14 N^3 per iteration
+    post_tf = post_flops / (ms_post / 1000.0) / 1e12
+    cap, cap_src = _ncu_capture()
+
+    def _traffic(key):
+        return _dram_bytes(cap[key]) if cap and key in cap else None
+
+    # end to end: sum over the step's kernels of (algorithmic work / peak) against the wall time
+    # of one step (the fraction of the step the machine would need at every kernel's roofline)
+    ideal_ms = {"eri": 1000.0 * flops / 1e12 / peak.value,
+                "xc": ITERS * 1000.0 * xc_flops / 1e12 / peak32.value,
+                "jk": ITERS * 1000.0 * info["eri_bytes"] / 1e9 / hbm_peak,
+                "post": ITERS * 1000.0 * post_flops / 1e12 / peak.value}
     n_ao_mean = float(np.mean(plan.pk.mol_nao))
     npp_m = nao * (nao + 1) / 2
     n_ao_ints = float(np.sum(npp_m * (npp_m + 1) / 2))
@@ -386,7 +423,7 @@ def run_ours(args, ws, rank, local):
         "roofline": {"kernel": "ERI stage (k_pairs, k_schwarz, 6 x k_eri)", "bound": "fp64",
                      "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
                      "frac": achieved / peak.value if peak.value else None,
-                     "traffic": _eri_traffic(),
+                     "traffic": _traffic("eri_256mol"), "traffic_source": cap_src,
                      "algorithmic": "SURVEY 8(d): 81 x F(class) per split-shell quartet surviving "
                                     f"Schwarz {opts.screen_eps:g}; {nq} quartets, {flops / 1e12:.3f} TFLOP per step",
                      "peak_source": "measured: dftb_fma_peak FP64 FMA probe on this GPU "
@@ -396,14 +433,26 @@ def run_ours(args, ws, rank, local):
         "roofline_xc": {"kernel": "k_xc (AO values + density + B3LYP + V_xc, f32 contractions)", "bound": "fp32",
                         "achieved": xc_tf, "peak": peak32.value, "unit": "TFLOP/s",
                         "frac": xc_tf / peak32.value if peak32.value else None, "ms_per_iteration": ms_xc,
+                        "traffic": _traffic("xc_256mol"),
                         "algorithmic": "4 N^2 flops per grid point per iteration (phi^T rho and phi wv^T), "
                                        f"{xc_flops / 1e9:.1f} GFLOP per iteration",
                         "peak_source": "measured: dftb_fma_peak FP32 FFMA probe on this GPU"},
         "roofline_jk": {"kernel": "k_jk (J/K digestion of the ERI store)", "bound": "hbm",
                         "achieved": jk_gbs, "peak": hbm_peak, "unit": "GB/s",
                         "frac": jk_gbs / hbm_peak if hbm_peak else None, "ms_per_iteration": ms_jk,
+                        "traffic": _traffic("jk_256mol"),
                         "algorithmic": f"the {info['eri_bytes'] / 2**30:.2f} GiB ERI store read once per iteration",
                         "peak_source": hbm_src},
+        "roofline_post": {"kernel": "k_post (Fock, energies, DIIS, density projector; one CTA per molecule)",
+                          "bound": "fp64", "achieved": post_tf, "peak": peak.value, "unit": "TFLOP/s",
+                          "frac": post_tf / peak.value if peak.value else None, "ms_per_iteration": ms_post,
+                          "traffic": _traffic("post_256mol"),
+                          "algorithmic": "SURVEY 8(d): 23 N^3 flops per molecule per iteration (9 N^3 "
+                                         f"diagonalisation + 14 N^3 products), {post_flops / 1e9:.2f} GFLOP per iteration",
+                          "timing": "re-run as a non-final iteration on the resident state (CUDA events)"},
+        "roofline_end_to_end": {"frac": sum(ideal_ms.values()) / ms, "ideal_ms_per_step": ideal_ms,
+                                "note": "sum over the step's kernels of algorithmic work / peak (ERI fp64, XC "
+                                        f"fp32, J/K HBM, post fp64; {ITERS} iterations) / measured ms per step"},
         "roofline_isolated": {"achieved": achieved_iso, "peak": peak.value, "unit": "TFLOP/s",
                               "frac": achieved_iso / peak.value if peak.value else None,
                               "timing": "same ERI stage, one batch alone on the GPU (warm-up pass)"},

@@ -187,6 +187,10 @@ int dftb_fma_peak(int fp64, double *tflops, void *stream);
  * one J/K launch set and of one XC launch set (ms).  Requires a completed dftb_plan_run, or
  * (ms_xc == NULL: J/K only) a dense store from dftb_plan_eri and a density from dftb_plan_jk. */
 int dftb_plan_kernel_times(dftb_plan *plan, int32_t reps, double *ms_jk, double *ms_xc, void *stream);
+/* Kernel-level timing of the post kernel (Fock, energies, DIIS, density projector) re-run as a
+ * non-final SCF iteration on the resident state.  Advances the plan's SCF state: call it
+ * only after the results were fetched. */
+int dftb_plan_post_time(dftb_plan *plan, int32_t reps, double *ms, void *stream);
 
 #ifdef __cplusplus
 }

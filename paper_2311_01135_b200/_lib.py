@@ -106,6 +106,7 @@ SIGNATURES = {
     "dftb_plan_set_full_eig": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "dftb_fma_peak": (ctypes.c_int, [ctypes.c_int, c_f64p, ctypes.c_void_p]),
     "dftb_plan_kernel_times": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, c_f64p, c_f64p, ctypes.c_void_p]),
+    "dftb_plan_post_time": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, c_f64p, ctypes.c_void_p]),
 }
 
 

@@ -1207,6 +1207,34 @@ int dftb_plan_kernel_times(dftb_plan *p, int32_t reps, double *ms_jk, double *ms
     return 0;
 }
 
+int dftb_plan_post_time(dftb_plan *p, int32_t reps, double *ms, void *stream) {
+    if (!p || reps < 1 || !ms) return fail(DFTB_EINVAL, "bad arguments");
+    if (p->opts.max_iterations < 2) return fail(DFTB_EINVAL, "needs max_iterations >= 2");
+    cudaStream_t st = (cudaStream_t)stream;
+    enq_begin(p, st);
+    const DevBatch &d = p->d;
+    const dftb_opts &o = p->opts;
+    const int it = o.max_iterations - 2;        // a non-final iteration: the purification path
+    CK(cudaMemsetAsync(d.done, 0, sizeof(int) * d.n_mol, st));
+    launch_post(d, p->nmax, it, o.diis_start, o.diis_history, o.damping_factor, o.convergence_std, st);   // warm
+    cudaEvent_t e[2];
+    for (auto &x : e) CK(cudaEventCreate(&x));
+    CK(cudaEventRecord(e[0], st));
+    for (int r = 0; r < reps; ++r) {
+        CK(cudaMemsetAsync(d.done, 0, sizeof(int) * d.n_mol, st));
+        launch_post(d, p->nmax, it, o.diis_start, o.diis_history, o.damping_factor, o.convergence_std, st);
+    }
+    CK(cudaEventRecord(e[1], st));
+    CK(cudaEventSynchronize(e[1]));
+    float a = 0.f;
+    CK(cudaEventElapsedTime(&a, e[0], e[1]));
+    *ms = a / reps;
+    for (auto &x : e) cudaEventDestroy(x);
+    CK(cudaGetLastError());
+    enq_end(p, st);
+    return 0;
+}
+
 int dftb_fma_peak(int fp64, double *tflops, void *stream) {
     *tflops = fma_peak(fp64, (cudaStream_t)stream);
     CK(cudaGetLastError());

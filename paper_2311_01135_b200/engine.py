@@ -123,6 +123,13 @@ class Plan:
                                                    ctypes.byref(x) if xc else None, self.stream))
         return jk.value, (x.value if xc else None)
 
+    def post_time(self, reps: int = 5) -> float:
+        """ms per launch of the post kernel re-run as a non-final iteration (dftb_plan_post_time;
+        advances the SCF state - after fetch only)."""
+        ms = ctypes.c_double(0.0)
+        _lib.check(self.lib.dftb_plan_post_time(self.h, int(reps), ctypes.byref(ms), self.stream))
+        return ms.value
+
     def eri(self, screened: bool = True):
         """Operator stage: pair tables, Schwarz bounds and the dense ERI store (dftb_plan_eri)."""
         _lib.check(self.lib.dftb_plan_eri(self.h, 1 if screened else 0, self.stream))
