@@ -49,7 +49,7 @@ __device__ __forceinline__ Arena carve(unsigned char *base, int nm, int hs = 10)
     a.cs = p; p += 2 * NPH;
     a.sn = p; p += 2 * NPH;
     a.dv = p; p += NMAX;
-    a.Bs = p; p += hs * hs;
+    a.Bs = p; p += hs * hs > 32 ? hs * hs : 32;     // also the Lanczos coefficients (2 x 16)
     a.cf = p; p += hs;
     a.red = p; p += 64;
     a.scal = p; p += 16;
@@ -62,7 +62,8 @@ __device__ __forceinline__ Arena carve(unsigned char *base, int nm, int hs = 10)
 }
 
 size_t scf_smem_bytes(int nm, int hs = 10) {
-    return sizeof(double) * ((size_t)nm * nm + arena_b(nm) + 4 * NPH + NMAX + (size_t)hs * hs + hs + 64 + 16) +
+    return sizeof(double) * ((size_t)nm * nm + arena_b(nm) + 4 * NPH + NMAX + (size_t)(hs * hs > 32 ? hs * hs : 32) +
+                             hs + 64 + 16) +
            sizeof(int) * (4 * NPH + NMAX);
 }
 
@@ -366,7 +367,7 @@ __device__ void sort_dv(int n, const Arena &ar) {
 // the Gershgorin bounds [lo, hi]) into [0, 1] with the occupied levels on top, and each step
 // replaces X by X^2 or 2X - X^2 - whichever trace lands closer to n_occ - which drives the
 // n_occ highest eigenvalues of X to 1 and the rest to 0 with the eigenvectors unchanged.  It
-// converges quadratically once the HOMO-LUMO gap is resolved; we stop two steps after the
+// converges quadratically once the HOMO-LUMO gap is resolved; we stop one step after the
 // idempotency error tr(X - X^2) = sum l(1 - l) falls below 1e-11, i.e. at round-off
 // (|l(1 - l)| < 1e-22).  One symmetric square per step (upper 4 x 4 tiles, Y in B) and two
 // CTA barriers: ~20-30 steps against the 3-10 Jacobi sweeps of N - 1 rotation steps each.
@@ -374,11 +375,136 @@ __device__ void sort_dv(int n, const Arena &ar) {
 // e.g. for a vanishing gap, where the projector is not defined by the spectrum alone.
 constexpr int TC2_MAX = 100;
 
-__device__ bool cta_tc2(double *X, double *Y, int M, int nocc, const Arena &ar, int *nsteps) {
+// Extreme-eigenvalue bounds of the symmetric M x M matrix A (shared memory) from LZ_STEPS
+// Lanczos steps (start vector (1, 1.01, 1.02, ...), no reorthogonalisation: lost orthogonality
+// only duplicates converged extreme Ritz values): [theta_min - beta_K - m, theta_max + beta_K + m],
+// beta_K the last Lanczos coefficient (the norm of the factorisation's residual, the Zhou-Saad
+// bound) and m = 1% of the Ritz width.  Multisection instead of a serial bisection: the f64
+// divisions of 100 Sturm sequences on one thread cost more than ten purification steps.  The Gershgorin bounds (F' spans about 4x its spectrum
+// for these molecules: [-55, 36] vs [-24.4, 0.6] Ha) cost the purification ~40% more steps; if
+// a bound were ever too tight the purification's convergence test fails and the caller
+// diagonalises.  Ritz values of the K x K tridiagonal by Sturm multisection (warps 0 / 1).
+constexpr int LZ_STEPS = 16;
+
+__device__ int sturm_count(const double *al, const double *be, int K, double x) {
+    // number of eigenvalues of the tridiagonal (al, be) below x
+    int c = 0;
+    double d = 1.0;
+    for (int k = 0; k < K; ++k) {
+        d = al[k] - x - (k ? be[k - 1] * be[k - 1] / d : 0.0);
+        if (d == 0.0) d = -1e-300;
+        c += d < 0.0;
+    }
+    return c;
+}
+
+// CTA sum with one barrier: warp partials into one of two alternating halves of red (a half is
+// rewritten only two reductions later, after every thread has read it), then every thread adds
+// the partials itself in the same order
+__device__ __forceinline__ double cta_sum1(double v, double *red, int &par) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    v = warp_sum(v);
+    double *r = red + (par ? 32 : 0);
+    par ^= 1;
+    if (lane == 0) r[w] = v;
+    __syncthreads();
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < SCF_THREADS / 32; ++k) t += r[k];
+    return t;
+}
+
+__device__ void lanczos_bounds(const double *A, int M, const Arena &ar, double *lo, double *hi) {
     const int tid = threadIdx.x, nt = SCF_THREADS;
+    double *al = ar.Bs, *be = ar.Bs + LZ_STEPS;        // alpha, beta (Bs >= 32 doubles)
+    double *v = ar.B, *vp = ar.B + NMAX, *w = ar.B + 2 * NMAX;   // B is free here (Y comes later)
+    int par = 0;
+    double nrm = 0.0;
+    for (int i = tid; i < M; i += nt) {
+        const double x = 1.0 + 0.01 * i;
+        vp[i] = 0.0;
+        nrm += x * x;
+    }
+    nrm = cta_sum1(nrm, ar.red, par);
+    const double inv = 1.0 / sqrt(nrm);
+    for (int i = tid; i < M; i += nt) v[i] = (1.0 + 0.01 * i) * inv;
+    __syncthreads();
+    int K = 0;
+    double bprev = 0.0;
+    const int part = tid & 3;
+    for (int k = 0; k < LZ_STEPS && k < M; ++k) {
+        // w = A v: four threads per row, interleaved columns, combined by shuffles
+        double a = 0.0;
+        for (int r = tid >> 2; r < ((M + 63) & ~63); r += nt / 4) {
+            double s = 0.0;
+            if (r < M)
+                for (int j = part; j < M; j += 4) s = fma(A[r * M + j], v[j], s);
+            s += __shfl_xor_sync(0xffffffffu, s, 1);
+            s += __shfl_xor_sync(0xffffffffu, s, 2);
+            if (r < M && part == 0) {
+                w[r] = s;
+                a += s * v[r];
+            }
+        }
+        a = cta_sum1(a, ar.red, par);                  // also orders the w writes
+        double b2 = 0.0;
+        for (int i = tid; i < M; i += nt) {
+            const double x = w[i] - a * v[i] - bprev * vp[i];
+            w[i] = x;
+            b2 += x * x;
+        }
+        b2 = cta_sum1(b2, ar.red, par);
+        const double bk = sqrt(b2);
+        if (tid == 0) { al[k] = a; be[k] = bk; }
+        K = k + 1;
+        bprev = bk;
+        if (bk < 1e-12 * fabs(a) + 1e-300) break;     // invariant subspace: Ritz values exact
+        for (int i = tid; i < M; i += nt) {            // each thread rewrites only its own i
+            vp[i] = v[i];
+            v[i] = w[i] / bk;
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    // extreme Ritz values: warp 0 the smallest, warp 1 the largest, by 32-way multisection of
+    // the tridiagonal's Gershgorin interval (Sturm counts at 32 points per round, 4 rounds:
+    // width / 2^20, far below the margins added below)
+    if (tid < 64) {
+        const int lane = tid & 31, wk = tid >> 5;
+        double g0 = 1e300, g1 = -1e300;
+        for (int k = 0; k < K; ++k) {
+            const double r = (k ? fabs(be[k - 1]) : 0.0) + (k + 1 < K ? fabs(be[k]) : 0.0);
+            g0 = fmin(g0, al[k] - r);
+            g1 = fmax(g1, al[k] + r);
+        }
+        const int target = wk == 0 ? 1 : K;            // count below x reaches 1 / K
+        double x0 = g0, x1 = g1;
+        for (int round = 0; round < 4; ++round) {
+            const double h = (x1 - x0) / 33.0;
+            const double x = x0 + h * (lane + 1);
+            const unsigned ge = __ballot_sync(0xffffffffu, sturm_count(al, be, K, x) >= target);
+            // the count is monotone in x: the first lane reaching the target brackets the root
+            const int f = ge ? __ffs(ge) - 1 : 32;
+            const double nx0 = f == 0 ? x0 : x0 + h * f, nx1 = f == 32 ? x1 : x0 + h * (f + 1);
+            x0 = nx0;
+            x1 = nx1;
+        }
+        if (lane == 0) ar.scal[4 + wk] = wk == 0 ? x0 : x1;
+    }
+    __syncthreads();
+    const double tmin = ar.scal[4], tmax = ar.scal[5], m = 0.01 * (tmax - tmin) + fabs(bprev);
+    *lo = tmin - m;
+    *hi = tmax + m;
+    __syncthreads();
+}
+
+__device__ bool cta_tc2(double *X, double *Y, int M, int nocc, const Arena &ar, int *nsteps,
+                        long long *prof = nullptr) {
+    const int tid = threadIdx.x, nt = SCF_THREADS;
+    const long long c0 = clock64();
     const int T = (M + 3) >> 2;                       // tiles per dimension
     const int ntile = T * (T + 1) / 2;                // upper triangle (ta <= tb)
-    // spectral bounds (Gershgorin) and X0
+    // spectral bounds: Gershgorin, tightened by a short Lanczos run and X0
     double lo = -1e300, hi = -1e300;                  // lo holds -min
     for (int i = tid; i < M; i += nt) {
         double r = 0.0;
@@ -389,6 +515,12 @@ __device__ bool cta_tc2(double *X, double *Y, int M, int nocc, const Arena &ar, 
     }
     block_max2(lo, hi, ar.red);
     lo = -lo;
+    {
+        double llo, lhi;
+        lanczos_bounds(X, M, ar, &llo, &lhi);
+        lo = fmax(lo, llo);
+        hi = fmin(hi, lhi);
+    }
     const double sc = 1.0 / (hi - lo);
     for (int t = tid; t < M * M; t += nt) {
         const int r = t / M, c = t - r * M;
@@ -400,8 +532,15 @@ __device__ bool cta_tc2(double *X, double *Y, int M, int nocc, const Arena &ar, 
     tr = block_sum(tr, ar.red);                       // ends with a barrier: X0 complete
     int extra = -1, k = 0;
     bool ok = false;
+    const long long c1 = clock64();
     for (; k < TC2_MAX; ++k) {
-        // Y = X X (X symmetric: Y_ij = sum_l X_li X_lj), upper tiles, mirrored on write
+        // Y = X X (X symmetric: Y_ij = sum_l X_li X_lj), upper 4 x 4 tiles, mirrored on write.
+        // The four values of a tile column are read as two 16-byte loads (rows start on 16-byte
+        // boundaries: M even or odd, 8 M l + 32 t is a multiple of 16 only for even M, so odd M
+        // takes the scalar loads); the sum is bound by shared-memory wavefronts, and 8-byte
+        // loads of 15 distinct tile columns per warp cost ~4x the wavefronts of 16-byte ones.
+        // Lanes past M read neighbouring values (inside the arena) into products never stored.
+        const bool vec = (M & 1) == 0;
         for (int u = tid; u < ntile; u += nt) {
             int ta = 0, rem = u;
             while (rem >= T - ta) { rem -= T - ta; ++ta; }
@@ -412,18 +551,33 @@ __device__ bool cta_tc2(double *X, double *Y, int M, int nocc, const Arena &ar, 
             for (int a = 0; a < 4; ++a)
 #pragma unroll
                 for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
-            for (int l = 0; l < M; ++l) {
-                const double *xr = X + l * M;
-                double xi[4], xj[4];
+            if (vec) {
+                for (int l = 0; l < M; ++l) {
+                    const double *xr = X + l * M;
+                    const double2 p0 = *reinterpret_cast<const double2 *>(xr + i0);
+                    const double2 p1 = *reinterpret_cast<const double2 *>(xr + i0 + 2);
+                    const double2 q0 = *reinterpret_cast<const double2 *>(xr + j0);
+                    const double2 q1 = *reinterpret_cast<const double2 *>(xr + j0 + 2);
+                    const double xi[4] = {p0.x, p0.y, p1.x, p1.y}, xj[4] = {q0.x, q0.y, q1.x, q1.y};
 #pragma unroll
-                for (int a = 0; a < 4; ++a) {
-                    xi[a] = i0 + a < M ? xr[i0 + a] : 0.0;
-                    xj[a] = j0 + a < M ? xr[j0 + a] : 0.0;
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) acc[a][c] = fma(xi[a], xj[c], acc[a][c]);
                 }
+            } else {
+                for (int l = 0; l < M; ++l) {
+                    const double *xr = X + l * M;
+                    double xi[4], xj[4];
 #pragma unroll
-                for (int a = 0; a < 4; ++a)
+                    for (int a = 0; a < 4; ++a) {
+                        xi[a] = i0 + a < M ? xr[i0 + a] : 0.0;
+                        xj[a] = j0 + a < M ? xr[j0 + a] : 0.0;
+                    }
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) acc[a][c] = fma(xi[a], xj[c], acc[a][c]);
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) acc[a][c] = fma(xi[a], xj[c], acc[a][c]);
+                }
             }
             double dsum = 0.0;
 #pragma unroll
@@ -448,9 +602,10 @@ __device__ bool cta_tc2(double *X, double *Y, int M, int nocc, const Arena &ar, 
         tr = sq ? tr2 : 2.0 * tr - tr2;
         __syncthreads();
         if (extra < 0 && fabs(idem) < 1e-11) extra = 0;
-        if (extra >= 0 && ++extra > 2) { ok = true; ++k; break; }
+        if (extra >= 0 && ++extra > 1) { ok = true; ++k; break; }
     }
     *nsteps = k;
+    if (prof && tid == 0) { prof[0] += c1 - c0; prof[1] += clock64() - c1; }
     return ok && fabs(tr - nocc) < 1e-6;
 }
 
@@ -857,20 +1012,21 @@ __global__ void __launch_bounds__(SCF_THREADS, 2) k_post(DevBatch b, PostArgs pa
     // (9) F' = X^T F X; orbitals (last iteration / callback path) or the density projector
     cta_gemm(S2, N, Fuse, N, false, X, N, false, N, M, N, 1.0, 0.0, ar);     // F X  (N x M, ld N)
     cta_gemm(ar.A, M, X, N, true, S2, N, false, M, M, N, 1.0, 0.0, ar);      // X^T (F X)
+    tick(7);
     bool eig = last || b.full_eig;
     if (!eig) {
         int nst = 0;
-        if (cta_tc2(ar.A, ar.B, M, nocc, ar, &nst)) {
+        if (cta_tc2(ar.A, ar.B, M, nocc, ar, &nst, dbg ? dbg + 14 : nullptr)) {
             // rho_new = 2 X P' X^T
             cta_gemm(S2, N, X, N, false, ar.A, M, false, N, M, M, 1.0, 0.0, ar);   // X P'  (N x M)
             cta_gemm(S1, N, S2, N, false, X, N, true, N, N, M, 2.0, 0.0, ar);       // 2 (X P') X^T
-            if (tid == 0) { b.puri[m] = nst; b.cpv[m] = 0; }
+            if (tid == 0) { b.puri[m] = nst; b.cpv[m] = 0; if (dbg) dbg[4] += nst; }
         } else {
             eig = true;                               // no converged projector: diagonalise
             if (tid == 0) b.puri[m] = -nst;
             cta_gemm(ar.A, M, X, N, true, S2, N, false, M, M, N, 1.0, 0.0, ar);   // F' again
         }
-        tick(4);
+        tick(8);
     }
     if (eig) {
         const bool warm = b.cpv[m] != 0;
@@ -888,7 +1044,7 @@ __global__ void __launch_bounds__(SCF_THREADS, 2) k_post(DevBatch b, PostArgs pa
         int nsw = 0;
         const double *Ad = cta_jacobi(ar.A, ar.B, M, ar, &nsw, 40, b.prec ? 1e-8 : 1e-13);
         if (dbg && tid == 0) dbg[10] += nsw;
-        tick(4);
+        tick(9);
         sort_eigs(Ad, M, ar);
         tick(5);
         for (int t = tid; t < M * M; t += SCF_THREADS) {
