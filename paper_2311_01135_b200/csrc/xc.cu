@@ -83,6 +83,16 @@ __device__ __forceinline__ int swz(int row, int col) {
     return row * BP + ((((col >> 2) ^ (row >> 2)) & (BP / 4 - 1)) << 2) + (col & 3);
 }
 
+// W-typed shell record: exponents, c_s, c_p (3 each); the f32 build adds -a log2(e) and -2a
+// (3 each) so the AO loop is one ex2.approx and FMAs per primitive
+template <typename W> constexpr int xc_swn() { return sizeof(W) == 4 ? 15 : 9; }
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 template <typename W, int NQ, int BP>
 struct XCL {
     static constexpr int NP = 4 * NQ;
@@ -97,17 +107,18 @@ struct XCL {
     static constexpr size_t shd = dw + ((sizeof(W) * 4 * BP + 15) & ~(size_t)15);
     // shell records: centres [nsh][3] f64 (for the point - centre difference), exponents and
     // coefficients [nsh][9] in W (no per-use f64 -> f32 conversions), (ao << 1 | kind) [nsh]
-    static size_t bytes(int nsh) { return shd + (XC_SHD_D * sizeof(double) + 9 * sizeof(W) + sizeof(int)) * (size_t)nsh; }
+    static size_t bytes(int nsh) { return shd + (XC_SHD_D * sizeof(double) + xc_swn<W>() * sizeof(W) + sizeof(int)) * (size_t)nsh; }
 };
 
 template <typename W, int NQ, int BP>
 __device__ __forceinline__ void xc_eval_phi(W *phi, const double *pt, const double *shd, const W *shw,
                                             const int *shi, int nsh, int nb) {
     constexpr int NP = 4 * NQ, PL = NP * BP;
+#pragma unroll 2
     for (int t = threadIdx.x; t < BP * nsh; t += XC_THREADS) {
         const int p = t % BP, sh = t / BP;
         const double *r = shd + XC_SHD_D * sh;
-        const W *f = shw + 9 * sh;
+        const W *f = shw + xc_swn<W>() * sh;
         const int kind = shi[sh] & 1, ao = shi[sh] >> 1;
         W v[4][4];  // [plane][component]
 #pragma unroll
@@ -130,18 +141,21 @@ __device__ __forceinline__ void xc_eval_phi(W *phi, const double *pt, const doub
             for (int k = 0; k < 3; ++k) {
                 const W a = f[k];
                 const W ar = a * r2;
-                W e;
+                W e, m2a;
                 if constexpr (sizeof(W) == 4) {
                     if (XC_AO_EXP) {
                         const double ard = r[3 + k] * r2d;
                         e = ard < (double)kCut ? expneg_f32acc(ard) : (W)0;
                     } else {
-                        e = ar < kCut ? expf(-ar) : (W)0;
+                        // exp(-a r^2) = 2^(-a log2(e) r^2); ex2.approx (~2 ulp) flushes the
+                        // underflowing primitives to zero, as the cut-off did
+                        e = ex2_approx(f[9 + k] * r2);
                     }
+                    m2a = f[12 + k];
                 } else {
                     e = ar < kCut ? exp(-ar) : (W)0;
+                    m2a = (W)-2 * a;
                 }
-                const W m2a = (W)-2 * a;
                 bs += f[3 + k] * e;
                 ds += f[3 + k] * m2a * e;
                 bp += f[6 + k] * e;
@@ -194,7 +208,7 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
     W *dw = (W *)(xsm + L::dw);
     double *shd = (double *)(xsm + L::shd);
     W *shw = (W *)(shd + XC_SHD_D * nsh);
-    int *shi = (int *)(shw + 9 * nsh);
+    int *shi = (int *)(shw + xc_swn<W>() * nsh);
     const int tid = threadIdx.x;
     const double *rg = b.rho + b.m_mat0[m];
     for (int t = tid; t < NP * NP; t += XC_THREADS) {
@@ -205,7 +219,7 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
     for (int sh = tid; sh < nsh; sh += XC_THREADS) {
         const int gsh = s0 + sh;
         double *r = shd + XC_SHD_D * sh;
-        W *f = shw + 9 * sh;
+        W *f = shw + xc_swn<W>() * sh;
         const double *A = b.a_xyz + 3 * b.s_atom[gsh];
         for (int d = 0; d < 3; ++d) {
             r[d] = A[d];
@@ -213,6 +227,10 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
             f[d] = (W)b.s_exp[3 * gsh + d];
             f[3 + d] = (W)b.s_cs[3 * gsh + d];
             f[6 + d] = (W)b.s_cp[3 * gsh + d];
+            if constexpr (sizeof(W) == 4) {
+                f[9 + d] = (W)(-1.4426950408889634 * b.s_exp[3 * gsh + d]);
+                f[12 + d] = (W)(-2.0 * b.s_exp[3 * gsh + d]);
+            }
         }
         shi[sh] = (b.s_ao[gsh] << 1) | (b.s_kind[gsh] & 1);
     }
@@ -240,21 +258,26 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
 #else
 #define XP(k) do { } while (0)
 #endif
+    // the points of a sub-block are loaded into pt[] during the previous sub-block's V phase
+    // (pt is not read there), so the global-load latency is off the critical path
+    auto load_pts = [&](int64_t sb_) {
+        if (tid < BP && sb_ < p1) {
+            const int nb_ = (int)min((int64_t)BP, p1 - sb_);
+            const int64_t gi = sb_ + min(tid, nb_ - 1);
+            pt[4 * tid] = b.g_xyz[3 * gi];
+            pt[4 * tid + 1] = b.g_xyz[3 * gi + 1];
+            pt[4 * tid + 2] = b.g_xyz[3 * gi + 2];
+            pt[4 * tid + 3] = tid < nb_ ? b.g_w[gi] : 0.0;
+        }
+    };
+    load_pts(p0);
     for (int64_t sb = p0; sb < p1; sb += BP) {
         const int nb = (int)min((int64_t)BP, p1 - sb);
 #ifdef XC_PHASES
         ++nsub;
 #endif
-        __syncthreads();                                   // previous sub-block consumed
+        __syncthreads();                                   // previous sub-block consumed, pt loaded
         XP(5);
-        if (tid < BP) {
-            const int64_t gi = sb + min(tid, nb - 1);
-            pt[4 * tid] = b.g_xyz[3 * gi];
-            pt[4 * tid + 1] = b.g_xyz[3 * gi + 1];
-            pt[4 * tid + 2] = b.g_xyz[3 * gi + 2];
-            pt[4 * tid + 3] = tid < nb ? b.g_w[gi] : 0.0;
-        }
-        __syncthreads();
         XP(0);
         xc_eval_phi<W, NQ, BP>(phi, pt, shd, shw, shi, nsh, nb);
         __syncthreads();
@@ -437,6 +460,7 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
         }
         __syncthreads();
         XP(4);
+        load_pts(sb + BP);
 #pragma unroll
         for (int j = 0; j < TJ; ++j) {                     // ---- V += phi wv^T, 4 x 4 tiles
             const int T = tid + j * XC_THREADS;
