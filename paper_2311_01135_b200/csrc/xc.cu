@@ -114,9 +114,12 @@ template <typename W, int NQ, int BP>
 __device__ __forceinline__ void xc_eval_phi(W *phi, const double *pt, const double *shd, const W *shw,
                                             const int *shi, int nsh, int nb) {
     constexpr int NP = 4 * NQ, PL = NP * BP;
+    static_assert(XC_THREADS % BP == 0, "a thread keeps one point for all its shells");
+    const int p = threadIdx.x % BP;                    // this thread's point (fixed), in registers
+    const double qx = pt[4 * p], qy = pt[4 * p + 1], qz = pt[4 * p + 2];
 #pragma unroll 2
     for (int t = threadIdx.x; t < BP * nsh; t += XC_THREADS) {
-        const int p = t % BP, sh = t / BP;
+        const int sh = t / BP;
         const double *r = shd + XC_SHD_D * sh;
         const W *f = shw + xc_swn<W>() * sh;
         const int kind = shi[sh] & 1, ao = shi[sh] >> 1;
@@ -126,8 +129,7 @@ __device__ __forceinline__ void xc_eval_phi(W *phi, const double *pt, const doub
 #pragma unroll
             for (int c = 0; c < 4; ++c) v[a][c] = (W)0;
         if (p < nb) {
-            const double *q = pt + 4 * p;
-            const double dxd = q[0] - r[0], dyd = q[1] - r[1], dzd = q[2] - r[2];
+            const double dxd = qx - r[0], dyd = qy - r[1], dzd = qz - r[2];
             const double r2d = dxd * dxd + dyd * dyd + dzd * dzd;
             const W dx = (W)dxd, dy = (W)dyd, dz = (W)dzd;
             const W r2 = (W)r2d;
