@@ -54,6 +54,15 @@ __device__ __forceinline__ void bulk_copy(void *dst, const void *src, uint32_t b
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// L2 prefetch of a byte range (no shared memory, no completion): the chunk after the one
+// being copied is pulled into L2 while the current one is digested, so the next bulk copy,
+// issued only when a stage buffer frees up, reads L2 instead of HBM
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+#ifndef JK_PREFETCH
+#define JK_PREFETCH 1      // chunks of look-ahead prefetched into L2 (0: off; 1: 1.284 -> 1.232 ms, 2: 1.238, 4: 1.254)
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
         "{\n .reg .pred p;\n"
@@ -438,6 +447,17 @@ __global__ void __launch_bounds__(32 * jk32_warps<NB>(), NB > 64 ? 1 : 3) k_jk32
         bulk_copy(stage + (size_t)slot * CR * LMAX, eri + eri_row(pi, pj), (uint32_t)(nr * L * 4), bar + slot);
         pj += CR;
         if (pj > pi) { --pi; pj = 0; }
+        if (JK_PREFETCH > 0) {        // the chunk JK_PREFETCH ahead of the next one, into L2
+            int qi = pi, qj = pj;
+            for (int k = 0; k < JK_PREFETCH && qi >= i0; ++k) {
+                qj += CR;
+                if (qj > qi) { --qi; qj = 0; }
+            }
+            if (qi >= i0) {
+                const int qr = min(CR, qi + 1 - qj);
+                bulk_prefetch_l2(eri + eri_row(qi, qj), (uint32_t)(qr * eri_rowlen(qi) * 4));
+            }
+        }
     };
     if (tid == 0) {
         for (int k = 0; k < NBUF; ++k) mbar_init(bar + k, 1);
