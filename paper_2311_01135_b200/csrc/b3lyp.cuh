@@ -30,6 +30,13 @@ constexpr double BETA = 0.0042;
 constexpr double VA = 0.0310907, VB = 13.0720, VC = 42.7198, VX0 = -0.409286;
 constexpr double LA = 0.04918, LB = 0.132, LC = 0.2533, LD = 0.349;
 constexpr double CF = 2.871234000188191;         // 0.3 (3 pi^2)^(2/3)
+// derived constants, the correctly rounded values of the reference's expressions (xc.py:237-252)
+constexpr double VQ = 0.0448998886415768;        // sqrt(4 VC - VB^2)
+constexpr double VX0F = 37.537128437796;         // VX0^2 + VB VX0 + VC
+constexpr double V2BQ = 582.2731590427809;       // 2 VB / Q
+constexpr double VBX0 = -0.14253052416798392;    // VB VX0 / X(x0)
+constexpr double V2BXQ = 545.8110641572265;      // 2 (VB + 2 VX0) / Q
+constexpr double CBRT_HALF = 0.7937005259840998; // 2^(-1/3)
 }  // namespace b3c
 
 HD XPart b3lyp_x(double n, double sigma) {
@@ -42,8 +49,8 @@ HD XPart b3lyp_x(double n, double sigma) {
     o.v0 = (4.0 / 3.0) * el;
     // Becke 88 on the spin density ns = n/2, sigma_s = sigma/4
     const double ns = 0.5 * n;
-    const double t = cbrt(ns), t4 = t * t * t * t;
-    const double x = sqrt(0.25 * sigma) / t4;
+    const double t = c13 * CBRT_HALF, t4 = t * t * t * t;   // (n/2)^(1/3) from n^(1/3)
+    const double x = 0.5 * sqrt(sigma) / t4;
     const double ash = asinh(x);
     const double den = 1.0 + 6.0 * BETA * x * ash;
     const double dden = 6.0 * BETA * (ash + x / sqrt(1.0 + x * x));
@@ -60,14 +67,11 @@ HD VPart b3lyp_vwn(double n) {
     VPart o;
     const double rs = cbrt(3.0 / (4.0 * kPi_ * n));
     const double y = sqrt(rs);
-    const double Xy = rs + VB * y + VC;
-    const double X0 = VX0 * VX0 + VB * VX0 + VC;
-    const double Q = sqrt(4.0 * VC - VB * VB);
-    const double at = atan(Q / (2.0 * y + VB));
-    const double ec = VA * (log(y * y / Xy) + (2.0 * VB / Q) * at -
-                            (VB * VX0 / X0) * (log((y - VX0) * (y - VX0) / Xy) + (2.0 * (VB + 2.0 * VX0) / Q) * at));
-    const double dec = VA * (2.0 / y - 2.0 * (y + VB) / Xy -
-                             (VB * VX0 / X0) * (2.0 / (y - VX0) - 2.0 * (y + VB + VX0) / Xy));
+    const double Xy = rs + VB * y + VC, iXy = 1.0 / Xy;
+    const double at = atan(VQ / (2.0 * y + VB));
+    const double ym = y - VX0;
+    const double ec = VA * (log(y * y * iXy) + V2BQ * at - VBX0 * (log(ym * ym * iXy) + V2BXQ * at));
+    const double dec = VA * (2.0 / y - 2.0 * (y + VB) * iXy - VBX0 * (2.0 / ym - 2.0 * (y + VB + VX0) * iXy));
     o.f2 = ec * n;
     o.v2 = ec - (rs / 3.0) * dec / (2.0 * y);
     return o;
@@ -78,18 +82,18 @@ HD LPart b3lyp_lyp(double n, double sigma) {
     LPart o;
     const double c13 = cbrt(n);
     const double tt = 1.0 / c13;                   // n^(-1/3)
-    const double Xd = 1.0 + LD * tt;
+    const double Xd = 1.0 + LD * tt, iXd = 1.0 / Xd;
     double tt2 = tt * tt, tt4 = tt2 * tt2, tt8 = tt4 * tt4;
-    const double om = tt8 * tt2 * tt * exp(-LC * tt) / Xd;   // t^11 e^{-c t} / X
-    const double dl = tt * (LC + LD / Xd);
-    const double n143 = n * n * n * n * cbrt(n * n);           // n^(14/3)
+    const double om = tt8 * tt2 * tt * exp(-LC * tt) * iXd;  // t^11 e^{-c t} / X
+    const double dl = tt * (LC + LD * iXd);
+    const double n143 = n * n * n * n * (c13 * c13);           // n^(14/3)
     const double s37 = 3.0 + 7.0 * dl;
-    o.f3 = -LA * n / Xd - LA * LB * om * CF * n143 + LA * LB * om * n * n * sigma * s37 / 72.0;
+    o.f3 = -LA * n * iXd - LA * LB * om * CF * n143 + LA * LB * om * n * n * sigma * s37 / 72.0;
     o.w3 = LA * LB * om * n * n * s37 / 72.0;
     const double tp = -tt / (3.0 * n);
-    const double omp = om * tp * (11.0 / tt - LC - LD / Xd);
-    const double dlp = tp * (LC + LD / Xd - LD * LD * tt / (Xd * Xd));
-    o.v3 = -LA / Xd + LA * n * LD * tp / (Xd * Xd) -
+    const double omp = om * tp * (11.0 * c13 - LC - LD * iXd);
+    const double dlp = tp * (LC + LD * iXd - LD * LD * tt * (iXd * iXd));
+    o.v3 = -LA * iXd + LA * n * LD * tp * (iXd * iXd) -
            LA * LB * CF * (omp * n143 + om * (14.0 / 3.0) * n143 / n) +
            (LA * LB * sigma / 72.0) * (omp * n * n * s37 + 2.0 * n * om * s37 + 7.0 * om * n * n * dlp);
     return o;
