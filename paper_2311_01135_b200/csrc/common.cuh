@@ -130,7 +130,7 @@ struct DevBatch {
     int *cpv;                 // [n_mol] Cp holds the previous iteration's eigenvectors (warm start valid)
     int *puri;                // [n_mol] purification sweeps of the last non-final iteration (diagnostics)
     int full_eig;             // 1: eigendecomposition every iteration (host callback path)
-    const double *boys;       // [BOYS_NT*BOYS_NCOL]
+    const double *boys;       // [kBoysLMax + 1][BOYS_NT][8] per-order slices (md.cuh)
     int max_it;
     long long *dbg;           // [n_mol*16] phase cycle counters (diagnostics)
 };

@@ -26,8 +26,21 @@ inline double drsqrt(double x) { return 1.0 / sqrt(x); }
 
 constexpr double kPi = 3.14159265358979323846;
 constexpr double kTwoPi25 = 34.98683665524972;   // 2 * pi^2.5
+constexpr double kHalfSqrtPi = 0.88622692545275801;  // sqrt(pi) / 2
 constexpr int kBoysNcol = 16;
 constexpr double kBoysStep = 0.1;
+constexpr int kBoysNT = 431;
+constexpr int kBoysLMax = 4;     // highest Hermite order of any integral here: (pp|pp), L = 4
+// The device reads a per-order slice of the Boys table: slice L holds, for each T grid point,
+// the 7 Taylor coefficients F_L .. F_{L+6} (plus one pad) in one 64-byte row, so a lookup is
+// four aligned 16-byte loads of one row and a class of fixed L touches a 27.6 KB table (the
+// full 431 x 16 table is 55 KB, and its 56-byte windows straddle 128-byte lines).
+inline void boys_slices_host(const double *tab, double *sl) {
+    for (int L = 0; L <= kBoysLMax; ++L)
+        for (int it = 0; it < kBoysNT; ++it)
+            for (int j = 0; j < 8; ++j)
+                sl[((size_t)L * kBoysNT + it) * 8 + j] = j < 7 ? tab[it * kBoysNcol + L + j] : 0.0;
+}
 
 HD constexpr int nherm(int L) { return (L + 1) * (L + 2) * (L + 3) / 6; }
 // flat index of Hermite (t,u,v): grouped by order s = t+u+v, then a = u+v, then v
@@ -35,7 +48,8 @@ HD constexpr int hidx(int t, int u, int v) {
     return (t + u + v) * (t + u + v + 1) * (t + u + v + 2) / 6 + (u + v) * (u + v + 1) / 2 + v;
 }
 
-// F_0..F_L(T); tab = 431 x 16 table of F_m at T = 0.1 k (boys.cu).  Mirrors _kernels.py:48-68.
+// F_0..F_L(T); tab = the per-order slices of the 431 x 16 table of F_m at T = 0.1 k
+// (boys_slices_host).  Mirrors _kernels.py:48-68.
 // exp(-T) is evaluated once, before the branch: quartets of one warp mix small and large T,
 // and with an exp in each branch a divergent warp paid for two (for T >= 700 exp(-T) is
 // below 1e-304 and leaves the asymptotic recursion unchanged, as the former explicit zero did)
@@ -43,19 +57,32 @@ template <int L>
 HD void boys(double T, double *F, const double *tab) {
     const double et = exp(-T);
     if (T > 42.95) {
-        double f = 0.5 * sqrt(kPi / T);
-        double h = 0.5 / T;
+        // sqrt(pi / T) / 2 and 1 / (2T) from one reciprocal square root
+        const double rt = drsqrt(T);
+        double f = kHalfSqrtPi * rt;
+        double h = 0.5 * rt * rt;
         F[0] = f;
 #pragma unroll
         for (int m = 0; m < L; ++m) F[m + 1] = ((2 * m + 1) * F[m] - et) * h;
     } else {
         int it = (int)(T * 10.0 + 0.5);
         double dT = T - it * kBoysStep;
-        const double *row = tab + it * kBoysNcol + L;
+        const double *row = tab + ((size_t)L * kBoysNT + it) * 8;
+        double rw[8];
+#ifdef __CUDA_ARCH__
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const double2 v = __ldg(reinterpret_cast<const double2 *>(row) + j);
+            rw[2 * j] = v.x;
+            rw[2 * j + 1] = v.y;
+        }
+#else
+        for (int j = 0; j < 8; ++j) rw[j] = row[j];
+#endif
         double acc = 0.0;
 #pragma unroll
-        for (int j = 6; j > 0; --j) acc = (acc + row[j]) * (-dT) * (1.0 / j);
-        F[L] = acc + row[0];
+        for (int j = 6; j > 0; --j) acc = (acc + rw[j]) * (-dT) * (1.0 / j);
+        F[L] = acc + rw[0];
 #pragma unroll
         for (int m = L - 1; m >= 0; --m) F[m] = (2.0 * T * F[m + 1] + et) * (1.0 / (2 * m + 1));
     }

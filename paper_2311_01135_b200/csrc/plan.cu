@@ -113,8 +113,9 @@ static int ensure_boys(int dev, const double **out) {
     if (dev < 0 || dev >= 64) return fail(DFTB_EINVAL, "device index out of range");
     std::lock_guard<std::mutex> lock(g_boys_mu);
     if (!g_boys[dev]) {
-        std::vector<double> tab(BOYS_NT * BOYS_NCOL);
-        boys_table_host(tab.data());
+        std::vector<double> full(BOYS_NT * BOYS_NCOL), tab((size_t)(kBoysLMax + 1) * kBoysNT * 8);
+        boys_table_host(full.data());
+        boys_slices_host(full.data(), tab.data());
         double *p = nullptr;
         CK(cudaMalloc(&p, tab.size() * sizeof(double)));
         CK(cudaMemcpy(p, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));

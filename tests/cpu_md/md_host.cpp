@@ -79,8 +79,9 @@ void md_boys_table(double *tab) { boys_table_host(tab); }
 void md_molecule(int nsh, const int *kind, const int *ao, const double *xyz, const double *ex,
                  const double *cs, const double *cp, int n_ao, int natom, const double *axyz,
                  const int *az, double prim_cut, double *dense, double *S, double *T, double *Vm) {
-    std::vector<double> tab(431 * 16);
-    boys_table_host(tab.data());
+    std::vector<double> full(431 * 16), tab((size_t)(kBoysLMax + 1) * kBoysNT * 8);
+    boys_table_host(full.data());
+    boys_slices_host(full.data(), tab.data());
     std::vector<Shell> sh(nsh);
     for (int s = 0; s < nsh; ++s) {
         sh[s].kind = kind[s];
