@@ -32,6 +32,13 @@
 namespace dftb {
 
 constexpr int XC_THREADS = 256;
+#ifndef XC_TUNR
+#define XC_TUNR 2      // unroll of the t-phase K loop (4-row groups)
+#endif
+#ifndef XC_VUNR
+#define XC_VUNR 16     // unroll of the V-phase point loop (4-point groups; 1: 1.744 ms, 2: 1.722, 4: 1.713, 16 = full: 1.695)
+#endif
+constexpr int kXcTunr = XC_TUNR, kXcVunr = XC_VUNR;   // (pragma arguments are not macro-expanded)
 // XC_MMA=1: f32 build runs the N 49..64 bucket on the tcgen05 kernel k_xc_mma below (parity
 // tests green on B200; measured 2.49 ms vs 2.27 ms per iteration for the FFMA kernel, so the
 // FFMA kernel stays the default - see DESIGN.md section 6, "measured and rejected")
@@ -298,7 +305,7 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
                         for (int h = 0; h < 2; ++h)
 #pragma unroll
                             for (int c = 0; c < 4; ++c) t2[h][c] = make_float2(0.f, 0.f);
-#pragma unroll 2
+#pragma unroll kXcTunr
                         for (int kq = 0; kq < (N + 3) / 4; ++kq) {
                             const W *pr = phi + 4 * kq * BP + (((pg ^ kq) & (BP / 4 - 1)) << 2);
                             const W *rr = rho + 4 * kq * NP + 4 * q;
@@ -469,6 +476,7 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
             if (T < NT) {
                 const int qa = T / NQ, qb = T % NQ;
                 const W *pa = phi + 4 * qa * BP, *pb = wv + 4 * qb * BP;   // rows 4qa.., 4qb..
+#pragma unroll kXcVunr
                 for (int c4 = 0; c4 < BP / 4; ++c4) {
                     const int ca = ((c4 ^ qa) & (BP / 4 - 1)) << 2, cb = ((c4 ^ qb) & (BP / 4 - 1)) << 2;
                     W fa[4][4], fb[4][4];
