@@ -406,6 +406,10 @@ struct JKPlan32 {
 #ifndef JK32
 #define JK32 1   // 0: the f32 build digests through k_jk<float> (f64 products) - A/B only
 #endif
+#ifndef JK_QUNR
+#define JK_QUNR 1      // unroll of the f32 kernel's tile-visit loop
+#endif
+constexpr int kJkQUnr = JK_QUNR;
 template <int NB> constexpr int jk32_warps() { return NB > 64 ? 8 : 4; }
 
 // rho f32 row-major, stride NB, 16-byte chunks XOR-swizzled by the row's 4-block (the
@@ -498,6 +502,7 @@ __global__ void __launch_bounds__(32 * jk32_warps<NB>(), NB > 64 ? 1 : 3) k_jk32
                 const float *rhoJ = rho + j * NB;
                 double oJ[4] = {0, 0, 0, 0}, oI[4] = {0, 0, 0, 0}, jp = 0.0;
                 if (lane_ok) {
+#pragma unroll kJkQUnr
                     for (int q = s; q <= A; q += S) {
                         const bool rp = q <= a;
                         const int ta = rp ? a : q - 1, tb = rp ? q : a;   // tile (ta, tb)

@@ -38,7 +38,14 @@ constexpr int XC_THREADS = 256;
 #ifndef XC_VUNR
 #define XC_VUNR 16     // unroll of the V-phase point loop (4-point groups; 1: 1.744 ms, 2: 1.722, 4: 1.713, 16 = full: 1.695)
 #endif
+#ifndef XC_AOUNR
+#define XC_AOUNR 2     // unroll of the AO-value task loop
+#endif
+#ifndef XC_WVUNR
+#define XC_WVUNR 1     // unroll of the wv row loop
+#endif
 constexpr int kXcTunr = XC_TUNR, kXcVunr = XC_VUNR;   // (pragma arguments are not macro-expanded)
+constexpr int kXcAoUnr = XC_AOUNR, kXcWvUnr = XC_WVUNR;
 // XC_MMA=1: f32 build runs the N 49..64 bucket on the tcgen05 kernel k_xc_mma below (parity
 // tests green on B200; measured 2.49 ms vs 2.27 ms per iteration for the FFMA kernel, so the
 // FFMA kernel stays the default - see DESIGN.md section 6, "measured and rejected")
@@ -124,7 +131,7 @@ __device__ __forceinline__ void xc_eval_phi(W *phi, const double *pt, const doub
     static_assert(XC_THREADS % BP == 0, "a thread keeps one point for all its shells");
     const int p = threadIdx.x % BP;                    // this thread's point (fixed), in registers
     const double qx = pt[4 * p], qy = pt[4 * p + 1], qz = pt[4 * p + 2];
-#pragma unroll 2
+#pragma unroll kXcAoUnr
     for (int t = threadIdx.x; t < BP * nsh; t += XC_THREADS) {
         const int sh = t / BP;
         const double *r = shd + XC_SHD_D * sh;
@@ -462,6 +469,7 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
             static_assert(XC_THREADS % BP == 0, "fixed point per thread");
             const int p = tid % BP;
             const W d0 = dw[p], d1 = dw[BP + p], d2 = dw[2 * BP + p], d3 = dw[3 * BP + p];
+#pragma unroll kXcWvUnr
             for (int row = tid / BP; row < NP; row += XC_THREADS / BP) {
                 const int o = swz<BP>(row, p);
                 wv[o] = d0 * phi[o] + d1 * phi[PL + o] + d2 * phi[2 * PL + o] + d3 * phi[3 * PL + o];
