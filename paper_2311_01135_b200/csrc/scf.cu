@@ -502,6 +502,70 @@ __device__ void lanczos_bounds(const double *A, int M, const Arena &ar, double *
     __syncthreads();
 }
 
+// FP64 tensor cores (mma.sync m8n8k4 .f64, DMMA): 256 FMAs per warp instruction at the FP64
+// peak (tools/probe/dmma_probe: 37 TFLOP/s with 4 warps x 4 chains per SM, 26-cycle latency)
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d[0]), "+d"(d[1]) : "d"(a), "d"(b));
+}
+#ifndef TC2_DMMA
+#define TC2_DMMA 1     // purification squarings on the FP64 tensor cores
+#endif
+// Y = X X for symmetric X (M x M, shared memory, row stride M) over the full square of 8 x 8
+// output tiles: warp w owns an RW x CW block of tiles (rows RW (w / 2).., columns CW (w % 2)..),
+// so per K step of 4 it loads RW + CW fragments (the B fragment of column tile t is, X being
+// symmetric, the A fragment of row tile t: X[8t + g][k + q]) for RW * CW independent MMA
+// chains.  Zero-padded past M.  The diagonal goes to ar.dv.
+template <int RW, int CW>
+__device__ void cta_square_dmma_t(const double *X, double *Y, int M, const Arena &ar) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, q = lane & 3;
+    const int r0 = RW * (warp >> 1), c0 = CW * (warp & 1);
+    double acc[RW][CW][2];
+#pragma unroll
+    for (int a = 0; a < RW; ++a)
+#pragma unroll
+        for (int c = 0; c < CW; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+#pragma unroll 2
+    for (int k0 = 0; k0 < M; k0 += 4) {
+        const int kk = k0 + q;
+        const bool kv = kk < M;
+        double fa[RW], fb[CW];
+#pragma unroll
+        for (int a = 0; a < RW; ++a) {
+            const int r = 8 * (r0 + a) + g;
+            fa[a] = (kv && r < M) ? X[r * M + kk] : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+            const int r = 8 * (c0 + c) + g;
+            fb[c] = (kv && r < M) ? X[r * M + kk] : 0.0;
+        }
+#pragma unroll
+        for (int a = 0; a < RW; ++a)
+#pragma unroll
+            for (int c = 0; c < CW; ++c) dmma884(acc[a][c], fa[a], fb[c]);
+    }
+#pragma unroll
+    for (int a = 0; a < RW; ++a)
+#pragma unroll
+        for (int c = 0; c < CW; ++c)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int i = 8 * (r0 + a) + g, j = 8 * (c0 + c) + 2 * q + e;
+                if (i < M && j < M) {
+                    Y[i * M + j] = acc[a][c][e];
+                    if (i == j) ar.dv[i] = acc[a][c][e];
+                }
+            }
+}
+
+__device__ __forceinline__ void cta_square_dmma(const double *X, double *Y, int M, const Arena &ar) {
+    static_assert(SCF_THREADS == 256, "eight warps: a 4 x 2 grid of tile blocks");
+    if (M <= 64) cta_square_dmma_t<2, 4>(X, Y, M, ar);
+    else cta_square_dmma_t<3, 6>(X, Y, M, ar);
+}
+
 __device__ bool cta_tc2(double *X, double *Y, int M, int nocc, const Arena &ar, int *nsteps,
                         long long *prof = nullptr) {
     const int tid = threadIdx.x, nt = SCF_THREADS;
@@ -545,6 +609,8 @@ __device__ bool cta_tc2(double *X, double *Y, int M, int nocc, const Arena &ar, 
         // loads of 15 distinct tile columns per warp cost ~4x the wavefronts of 16-byte ones.
         // Lanes past M read neighbouring values (inside the arena) into products never stored.
         const bool vec = (M & 1) == 0;
+        if (TC2_DMMA) cta_square_dmma(X, Y, M, ar);
+        else
         for (int u = tid; u < ntile; u += nt) {
             int ta = 0, rem = u;
             while (rem >= T - ta) { rem -= T - ta; ++ta; }
@@ -601,7 +667,16 @@ __device__ bool cta_tc2(double *X, double *Y, int M, int nocc, const Arena &ar, 
         }
         __syncthreads();
         double tr2 = 0.0;
-        for (int a = 0; a < T; ++a) tr2 += ar.dv[a];    // same fixed order in every thread
+        if (TC2_DMMA) {
+            // every warp forms the same shuffle-tree sum (fixed order, no extra barrier; a
+            // serial 58-term sum in every thread cost ~1.5k cycles of shared-memory latency)
+            const int ln = tid & 31;
+            double t2 = 0.0;
+            for (int e = ln; e < M; e += 32) t2 += ar.dv[e];
+            tr2 = __shfl_sync(0xffffffffu, warp_sum(t2), 0);   // lane 0's (butterfly orders differ per lane)
+        } else {
+            for (int a = 0; a < T; ++a) tr2 += ar.dv[a];
+        }
         const bool sq = fabs(tr2 - nocc) <= fabs(2.0 * tr - tr2 - nocc);
         const double idem = tr - tr2;
         for (int t = tid; t < M * M; t += nt) X[t] = sq ? Y[t] : 2.0 * X[t] - Y[t];
