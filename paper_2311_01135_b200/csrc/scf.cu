@@ -72,8 +72,8 @@ size_t scf_smem_bytes(int nm, int hs = 10) {
 // 64 x 64 blocks (one for M, N <= 64): 16 x 16 threads with 4 x 4 register tiles, K in
 // panels of KP staged zero-padded into ar.sa / ar.sb ([KP][64] each), so the inner loop has
 // no bounds tests.  C must not alias A or B (blocks are written as they finish).
-__device__ void cta_gemm(double *C, int ldc, const double *A, int lda, bool tA, const double *B, int ldb,
-                         bool tB, int M, int N, int K, double alpha, double beta, const Arena &ar) {
+__device__ void cta_gemm_ffma(double *C, int ldc, const double *A, int lda, bool tA, const double *B, int ldb,
+                              bool tB, int M, int N, int K, double alpha, double beta, const Arena &ar) {
     const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
     double *const sa = ar.sa, *const sb = ar.sb;
     constexpr int SU = KP * 64 / SCF_THREADS;           // staged elements per thread per operand
@@ -147,6 +147,84 @@ __device__ void cta_gemm(double *C, int ldc, const double *A, int lda, bool tA, 
                 }
         }
     __syncthreads();
+}
+
+// FP64 tensor cores (mma.sync m8n8k4 .f64, DMMA): 256 FMAs per warp instruction at the FP64
+// peak (tools/probe/dmma_probe: 37 TFLOP/s with 4 warps x 4 chains per SM, 26-cycle latency)
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d[0]), "+d"(d[1]) : "d"(a), "d"(b));
+}
+
+// The same product on the FP64 tensor cores: warp w owns an RW x CW block of 8 x 8 output tiles
+// (rows RW (w / 2).., columns CW (w % 2)..), K in steps of 4; fragments read in place (global or
+// shared) with zero padding past M, N, K: A fragment element (i0 + g, k0 + q) of op(A), B
+// fragment element (k0 + q, j0 + g) of op(B), accumulator elements (i0 + g, j0 + 2q + e).
+template <int RW, int CW>
+__device__ void cta_gemm_dmma_t(double *C, int ldc, const double *A, int lda, bool tA, const double *B, int ldb,
+                                bool tB, int M, int N, int K, double alpha, double beta) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, q = lane & 3;
+    const int r0 = RW * (warp >> 1), c0 = CW * (warp & 1);
+    double acc[RW][CW][2];
+#pragma unroll
+    for (int a = 0; a < RW; ++a)
+#pragma unroll
+        for (int c = 0; c < CW; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+    const bool any = 8 * r0 < M && 8 * c0 < N;          // warp-uniform
+    if (any) {
+#pragma unroll 2
+        for (int k0 = 0; k0 < K; k0 += 4) {
+            const int kk = k0 + q;
+            const bool kv = kk < K;
+            double fa[RW], fb[CW];
+#pragma unroll
+            for (int a = 0; a < RW; ++a) {
+                const int i = 8 * (r0 + a) + g;
+                fa[a] = (kv && i < M) ? (tA ? A[(int64_t)kk * lda + i] : A[(int64_t)i * lda + kk]) : 0.0;
+            }
+#pragma unroll
+            for (int c = 0; c < CW; ++c) {
+                const int j = 8 * (c0 + c) + g;
+                fb[c] = (kv && j < N) ? (tB ? B[(int64_t)j * ldb + kk] : B[(int64_t)kk * ldb + j]) : 0.0;
+            }
+#pragma unroll
+            for (int a = 0; a < RW; ++a)
+#pragma unroll
+                for (int c = 0; c < CW; ++c) dmma884(acc[a][c], fa[a], fb[c]);
+        }
+    }
+    __syncthreads();                                     // every operand read before C is written
+#pragma unroll
+    for (int a = 0; a < RW; ++a)
+#pragma unroll
+        for (int c = 0; c < CW; ++c)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int i = 8 * (r0 + a) + g, j = 8 * (c0 + c) + 2 * q + e;
+                if (i < M && j < N) {
+                    double x = alpha * acc[a][c][e];
+                    if (beta != 0.0) x += beta * C[(int64_t)i * ldc + j];
+                    C[(int64_t)i * ldc + j] = x;
+                }
+            }
+    __syncthreads();
+}
+
+#ifndef GEMM_DMMA
+#define GEMM_DMMA 1    // the post kernel's GEMMs on the FP64 tensor cores
+#endif
+__device__ __forceinline__ void cta_gemm(double *C, int ldc, const double *A, int lda, bool tA, const double *B,
+                                         int ldb, bool tB, int M, int N, int K, double alpha, double beta,
+                                         const Arena &ar) {
+    if (GEMM_DMMA) {
+        static_assert(SCF_THREADS == 256, "eight warps: a 4 x 2 grid of tile blocks");
+        __syncthreads();                                 // operands written by the caller
+        if (M <= 64 && N <= 64) cta_gemm_dmma_t<2, 4>(C, ldc, A, lda, tA, B, ldb, tB, M, N, K, alpha, beta);
+        else cta_gemm_dmma_t<3, 6>(C, ldc, A, lda, tA, B, ldb, tB, M, N, K, alpha, beta);
+    } else {
+        cta_gemm_ffma(C, ldc, A, lda, tA, B, ldb, tB, M, N, K, alpha, beta, ar);
+    }
 }
 
 // Cyclic Jacobi, round-robin (circle) pairing: n/2 disjoint rotations per step,
@@ -502,12 +580,6 @@ __device__ void lanczos_bounds(const double *A, int M, const Arena &ar, double *
     __syncthreads();
 }
 
-// FP64 tensor cores (mma.sync m8n8k4 .f64, DMMA): 256 FMAs per warp instruction at the FP64
-// peak (tools/probe/dmma_probe: 37 TFLOP/s with 4 warps x 4 chains per SM, 26-cycle latency)
-__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                 : "+d"(d[0]), "+d"(d[1]) : "d"(a), "d"(b));
-}
 #ifndef TC2_DMMA
 #define TC2_DMMA 1     // purification squarings on the FP64 tensor cores
 #endif
