@@ -165,6 +165,24 @@ struct KetSmem {
     }
 };
 
+// Per-warp copy of the inner (ket) pair's nine primitive records (all 10 fields) when every
+// active lane of the warp has the same ket pair - the usual case with the transposed quartet
+// enumeration - else the records come from global memory.  Reads are shared-memory broadcasts
+// at constant offsets (no 64-bit address arithmetic per field).
+struct WarpKet {
+    const double *s;     // [10 fields][9 prims] of this warp, or null
+    PPView g;
+    __device__ __forceinline__ double get(int f, int k, int64_t pair) const {
+        return s ? s[f * 9 + k] : g.get(f, k, pair);
+    }
+};
+#ifndef ERI_WKC
+#define ERI_WKC 2        // per-warp ket records: 1 every class, 2 the classes without the per-thread cache
+#endif
+#ifndef ERI_WKC_PAD
+#define ERI_WKC_PAD 0    // A/B: extra shared memory for the classes that had the per-thread cache
+#endif
+
 // One thread = one screened shell quartet x one component slice (blockIdx.y).
 // KPS: inner-pair components per slice (0 = all): a slice recomputes the Boys function and
 // R_tuv of all 81 primitive quartets, so fewer slices trade registers for less recomputation.
@@ -201,7 +219,21 @@ __global__ void __launch_bounds__(ERI_T, MINB) k_eri(DevBatch b, int cls, double
     const PPView V{b.pp, b.n_pair};
     extern __shared__ double eri_ksm[];
     using KS = KetSmem<(KC || KD), NS>;
-    if constexpr (KSM) {
+    const double *wk = nullptr;
+    constexpr bool WK = ERI_WKC == 1 ? !SW : ERI_WKC == 2 ? (!SW && !KSM) : false;
+    if constexpr (WK) {
+        const unsigned mask = __activemask();
+        const int lane = threadIdx.x & 31, lead = __ffs(mask) - 1;
+        const int64_t q0 = __shfl_sync(mask, Qp, lead);
+        if (__all_sync(mask, Qp == q0)) {
+            double *ws = eri_ksm + (threadIdx.x >> 5) * 90;
+            const int nact = __popc(mask), rk = __popc(mask & ((1u << lane) - 1));
+            for (int e = rk; e < 90; e += nact) ws[e] = V.get(e / 9, e % 9, Qp);
+            __syncwarp(mask);
+            wk = ws;
+        }
+    }
+    if constexpr (KSM && !WK) {
 #pragma unroll
         for (int f = 0; f < KS::NSLOT; ++f) {
             const int field = KS::field(f);
@@ -221,6 +253,9 @@ __global__ void __launch_bounds__(ERI_T, MINB) k_eri(DevBatch b, int cls, double
             for (int y = 0; y < NKS; ++y) out[x][y] = 0.0;
         if constexpr (SW) {
             eri_quartet_kv<KC, KD, KA, KB, KC0, NKS>(V, V, Qp, Pp, C, D, A, B, b.boys, prim_cut, out);
+        } else if constexpr (WK) {
+            const WarpKet VK{wk, V};
+            eri_quartet_kv<KA, KB, KC, KD, KC0, NKS>(V, VK, Pp, Qp, A, B, C, D, b.boys, prim_cut, out);
         } else if constexpr (KSM) {
             const KS VK{eri_ksm, (int)threadIdx.x, V};
             eri_quartet_kv<KA, KB, KC, KD, KC0, NKS>(V, VK, Pp, Qp, A, B, C, D, b.boys, prim_cut, out);
@@ -323,7 +358,9 @@ static void launch_cls(const DevBatch &b, int cls, int64_t n, double eps, double
     if (!n) return;
     constexpr int NIN = SW ? (KA ? 4 : 1) * (KB ? 4 : 1) : (KC ? 4 : 1) * (KD ? 4 : 1);
     constexpr int NSL = NIN / (KPS ? KPS : NIN);
-    const size_t sm = KSM ? sizeof(double) * KetSmem<(KC || KD), NS>::NSLOT * 9 * ERI_T : 0;
+    constexpr bool WK = ERI_WKC == 1 ? !SW : ERI_WKC == 2 ? (!SW && !KSM) : false;
+    const size_t sm = WK ? sizeof(double) * 90 * (ERI_T / 32) + ERI_WKC_PAD * KSM
+                      : KSM ? sizeof(double) * KetSmem<(KC || KD), NS>::NSLOT * 9 * ERI_T : 0;
     auto kern = k_eri<KA, KB, KC, KD, KPS, ST, KSM, MINB, NS, SW>;
     smem_optin((const void *)kern);
     kern<<<dim3(nblk(n, ERI_T), NSL), ERI_T, sm, s>>>(b, cls, eps, prim_cut, eri);
