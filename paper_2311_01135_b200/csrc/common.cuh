@@ -31,6 +31,10 @@ HD int64_t pidx(int i, int j) { return i >= j ? tri(i) + j : tri(j) + i; }
 // k == i and l > j are zero (they belong to other rows).  All i + 1 rows of slab i have the
 // same length 16 * tri(i/4 + 1), so a row starts on a 64-byte (f32) / 128-byte (f64)
 // boundary and the J/K kernel can read whole tiles with 16-byte vector loads.
+// Inside a tile the four rows are rotated by eri_tile_rot(tile index): logical row r sits in
+// 4-element slot (r + rot) & 3.  A J/K thread that owns tile tau reads its rows in logical
+// order from slots (r + rot) & 3, so the 8 lanes of a quarter warp (8 consecutive tiles,
+// 64 bytes apart) hit 8 different 16-byte bank groups instead of 2 (a 4-way conflict).
 HD int64_t eri_rowlen(int i) {
     const int64_t A = (i >> 2) + 1;
     return 8 * A * (A + 1);
@@ -42,7 +46,12 @@ HD int64_t eri_slab0(int i) {                 // elements in all rows with first
     return full + eri_rowlen(i) * (tri(i) - tri(4 * a));
 }
 HD int64_t eri_row(int i, int j) { return eri_slab0(i) + (int64_t)j * eri_rowlen(i); }
-HD int eri_ket(int k, int l) { return 16 * (int)(tri(k >> 2) + (l >> 2)) + 4 * (k & 3) + (l & 3); }  // k >= l
+HD int eri_tile_rot(int tau) { return (tau >> 1) & 3; }
+HD int eri_tile_slot(int tau, int r) { return (r + eri_tile_rot(tau)) & 3; }    // 4-element slot of logical row r
+HD int eri_ket(int k, int l) {   // k >= l
+    const int tau = (int)(tri(k >> 2) + (l >> 2));
+    return 16 * tau + 4 * eri_tile_slot(tau, k & 3) + (l & 3);
+}
 // offset of (ij|kl) in a molecule's store (any index order)
 HD int64_t eri_pos(int i, int j, int k, int l) {
     if (i < j) { const int t = i; i = j; j = t; }

@@ -235,12 +235,13 @@ __global__ void __launch_bounds__(32 * jk_warps<NB>(), NB > 64 ? 2 : NB > 32 ? 3
                         const int beta = rp ? q : q - 1;                  // rho block of the product
                         const bool dg = ta == tb;
                         float tf[16];
+                        const int tq = tri32(ta) + tb, rot = eri_tile_rot(tq);   // rows sit in slots (r + rot) & 3
                         {
-                            const float4 *qp = reinterpret_cast<const float4 *>(row + 16 * (tri32(ta) + tb));
+                            const float4 *qp = reinterpret_cast<const float4 *>(row + 16 * tq);
                             if constexpr (sizeof(ST) == 4) {
 #pragma unroll
                                 for (int r = 0; r < 4; ++r) {
-                                    const float4 v = qp[r];
+                                    const float4 v = qp[(r + rot) & 3];
                                     tf[4 * r] = v.x; tf[4 * r + 1] = v.y; tf[4 * r + 2] = v.z; tf[4 * r + 3] = v.w;
                                 }
                                 if (dg) { tf[0] *= 0.5f; tf[5] *= 0.5f; tf[10] *= 0.5f; tf[15] *= 0.5f; }
@@ -255,10 +256,10 @@ __global__ void __launch_bounds__(32 * jk_warps<NB>(), NB > 64 ? 2 : NB > 32 ? 3
                                     t[4 * r + c] = (double)(rp ? tf[4 * r + c] : tf[4 * c + r]);
                         } else {
                             double td[16];
-                            const double2 *qp = reinterpret_cast<const double2 *>(row + 16 * (tri32(ta) + tb));
+                            const double2 *qp = reinterpret_cast<const double2 *>(row + 16 * tq);
 #pragma unroll
                             for (int r = 0; r < 8; ++r) {
-                                const double2 v = qp[r];
+                                const double2 v = qp[2 * (((r >> 1) + rot) & 3) + (r & 1)];
                                 td[2 * r] = v.x; td[2 * r + 1] = v.y;
                             }
 #pragma unroll
@@ -371,7 +372,7 @@ __global__ void __launch_bounds__(32 * jk_warps<NB>(), NB > 64 ? 2 : NB > 32 ? 3
             while (tri(a + 1) <= tau) ++a;
             while (tri(a) > tau) --a;
             const int bb = tau - (int)tri(a);
-            const int kk = 4 * a + ((e >> 2) & 3), ll = 4 * bb + (e & 3);
+            const int kk = 4 * a + ((((e >> 2) & 3) + 4 - eri_tile_rot(tau)) & 3), ll = 4 * bb + (e & 3);
             if (kk < N && ll <= kk) Js[tri(kk) + ll] = acc[k][v];
         }
 }
@@ -379,99 +380,131 @@ __global__ void __launch_bounds__(32 * jk_warps<NB>(), NB > 64 ? 2 : NB > 32 ? 3
 // ---------------------------------------------------------------------------- f32 build
 // The f32 build stores the ERI values and the density in f32 (the reference's f32 working
 // dtype, integrals.py:171, scf.py:169-174), so every product v * rho of the digestion is a
-// product of two f32 numbers.  k_jk32 forms those products on the packed FP32 pipe (FFMA2,
-// two lanes per instruction) in short f32 partial sums - four products per tile row / column
-// for K and J_P, one slab of rows for J_Q - and accumulates the partials in f64.  Relative to
-// the reference's exact f64 products that adds a rounding of ~2^-24 per partial, the size of
-// the f32 rounding already in every stored value.  Removes the per-element f32 -> f64
-// conversions (XU pipe) and DFMA of the f64 formulation; the digestion plan is the same as
-// k_jk's (one warp per row, lane group per 4-block a, A + 1 tile visits per block).
-template <int NB, int WARPS>
+// product of two f32 numbers.  k_jk32 forms those products on the packed FP32 pipe (FFMA2)
+// in short f32 partial sums - four products per tile row / column for K, one tile for J_P,
+// one slab of rows for J_Q - and accumulates the partials in f64 (the reference accumulates
+// in f64 and rounds J, K to f32 at the end).
+//
+// Tile owners.  A thread owns ONE tile position tau = (ta, tb) of the ket matrix for a whole
+// slab i and walks the slab's rows j (R rows in parallel when the row has fewer tiles than
+// the CTA has threads).  Everything that depends on the tile position only - the tile's
+// address, rho[ta-block][tb-block] for J_P, rho_i[ta], rho_i[tb], the J_Q accumulators of
+// the tile's 16 kets, the G_i partial sums of the tile's two 4-blocks - stays in registers
+// across the slab, so the inner loop over rows is loads, FFMA2 and pointer increments: no
+// index arithmetic, no divergence, no transposition selects.  Consecutive lanes own
+// consecutive tiles; with the rows of a tile rotated in the store (common.cuh) the four
+// 16-byte loads of a tile are bank-conflict free.  Each tile is read once and serves both
+// of its 4-blocks: the row part T rho[tb] (result block ta) and the column part T^T rho[ta]
+// (result block tb).
+// The one reduction across tiles that cannot stay in registers is G_j = 2 T_P rho_i (a
+// per-row result): the thread writes its two 4-vectors (and its J_P term) over the 64
+// bytes of the tile it has just consumed, and after a CTA barrier a reduce pass sums, for
+// every (row, 4-block), the A + 1 tile terms in a fixed order (f64) and issues the RED adds.
+// G_i and J_Q are reduced the same way once per slab, through the stage buffer of the slab's
+// last chunk.  Chunks of rows arrive by cp.async.bulk into two stage buffers (mbarrier
+// completion), the chunk after the one in flight is prefetched into L2.
+template <int NB> constexpr int jk32_threads() { return NB <= 80 ? 256 : 320; }
+
+template <int NB>
 struct JKPlan32 {
-    static constexpr int THREADS = 32 * WARPS;
+    static constexpr int THREADS = jk32_threads<NB>();
     static constexpr int AMAX = NB / 4;
-    static constexpr int LMAX = 8 * AMAX * (AMAX + 1);          // f32 elements of the longest row
-    static constexpr size_t row_bytes = (size_t)LMAX * 4;
-    // rho f32 [NB][NB] + J_Q accumulators f64 [LMAX] + G_i reduction [THREADS][4] f64
-    static constexpr size_t fixed = 128 + 4 * (size_t)NB * NB + 8 * (size_t)LMAX + 32 * (size_t)THREADS;
-    static constexpr size_t cap = 227 * 1024;
-    static constexpr int ctas(size_t bytes) { return (int)((228 * 1024) / (bytes + 1024)); }
-    static constexpr int NBUF =
-        fixed + 2 * WARPS * row_bytes <= cap && !(ctas(fixed + WARPS * row_bytes) > ctas(fixed + 2 * WARPS * row_bytes))
-            ? 2 : 1;
-    static constexpr int CR = fixed + NBUF * WARPS * row_bytes <= cap ? WARPS : WARPS / 2;
-    static constexpr size_t bytes = fixed + NBUF * CR * row_bytes;
-    static_assert(bytes <= cap, "J/K bucket does not fit in shared memory");
+    static constexpr int TMAX = AMAX * (AMAX + 1) / 2;          // tiles of the longest row
+    static constexpr int LMAX = 16 * TMAX;                       // f32 elements of the longest row
+    static constexpr int AP = AMAX <= 16 ? 16 : 32;              // reduce pass: lanes per row before the term split
+    static constexpr int RPASS = THREADS / AP;                   // rows one reduce pass can take
+    static_assert(THREADS >= TMAX, "one tile position per thread");
+    static constexpr size_t row_bytes = 4 * (size_t)LMAX;
+    // mbarriers | rho f32 [NB][NB] | J_Q f64 [LMAX] | corr1, corr2 f64 [NB] | (ij|ij) f32 [RPASS] |
+    // stage f32 [2][SFL]
+    static constexpr size_t o_rho = 128;
+    static constexpr size_t o_jq = o_rho + 4 * (size_t)NB * NB;
+    static constexpr size_t o_c1 = o_jq + 8 * (size_t)LMAX;
+    static constexpr size_t o_vp = o_c1 + 16 * (size_t)NB;
+    static constexpr size_t o_stage = (o_vp + 4 * (size_t)RPASS + 127) & ~(size_t)127;
+    static constexpr size_t cap2 = 113 * 1024, cap1 = 227 * 1024;   // per CTA at 2 / 1 CTAs per SM
+    static constexpr int rows2 = o_stage < cap2 ? (int)((cap2 - o_stage) / (2 * row_bytes)) : 0;
+    static constexpr int rows1 = (int)((cap1 - o_stage) / (2 * row_bytes));
+    static constexpr int CTAS = rows2 >= 4 ? 2 : 1;
+    static constexpr int rowsc = CTAS == 2 ? rows2 : rows1;
+    static constexpr int SROWS = rowsc < RPASS ? rowsc : RPASS; // longest rows per stage buffer
+    static_assert(SROWS >= 1, "J/K bucket does not fit in shared memory");
+    static constexpr int SFL = SROWS * LMAX;                     // f32 elements per stage buffer
+    static constexpr size_t bytes = o_stage + 8 * (size_t)SFL;
+    static_assert(bytes <= cap1, "J/K bucket does not fit in shared memory");
 };
-#ifndef JK32
-#define JK32 1   // 0: the f32 build digests through k_jk<float> (f64 products) - A/B only
-#endif
-#ifndef JK_QUNR
-#define JK_QUNR 1      // unroll of the f32 kernel's tile-visit loop
-#endif
-constexpr int kJkQUnr = JK_QUNR;
-template <int NB> constexpr int jk32_warps() { return NB > 64 ? 8 : 4; }
 
-// rho f32 row-major, stride NB, 16-byte chunks XOR-swizzled by the row's 4-block (the
-// lanes of a warp read the same column block of rows in different 4-blocks)
-// (XOR over the low 3 chunk-index bits when a row holds a multiple of 8 chunks, else 2, so
-// the permutation stays inside the row)
-template <int NB>
-__device__ __forceinline__ int sw32key(int r) { return (r >> 2) & ((NB / 4) % 8 == 0 ? 7 : 3); }
-template <int NB>
-__device__ __forceinline__ int rsw32(int r, int c) {
-    return r * NB + (((c >> 2) ^ sw32key<NB>(r)) << 2) + (c & 3);
-}
 __device__ __forceinline__ float4 lds4(const float *p) { return *reinterpret_cast<const float4 *>(p); }
+__device__ __forceinline__ float2 lo2(const float4 v) { return make_float2(v.x, v.y); }
+__device__ __forceinline__ float2 hi2(const float4 v) { return make_float2(v.z, v.w); }
+__device__ __forceinline__ float2 dup2(float x) { return make_float2(x, x); }
+// sum_c t[c] v[c] as two packed FMAs and one add (a 4-product f32 partial)
+__device__ __forceinline__ float dot4(const float4 t, const float4 v) {
+    float2 p = __ffma2_rn(lo2(t), lo2(v), make_float2(0.f, 0.f));
+    p = __ffma2_rn(hi2(t), hi2(v), p);
+    return p.x + p.y;
+}
+
+// chunking of slab i: nt tiles and L elements per row, R rows digested in parallel, CR rows per chunk
+struct JKSlab { int nt, L, R, CR; };
+template <int NB>
+__device__ __forceinline__ JKSlab jk32_slab(int i) {
+    using PL = JKPlan32<NB>;
+    JKSlab s;
+    const int A = (i >> 2) + 1;
+    s.nt = (A * (A + 1)) >> 1;
+    s.L = 16 * s.nt;
+    const int cr = min(PL::SFL / s.L, PL::RPASS);
+    s.R = min(PL::THREADS / s.nt, cr);
+    s.CR = cr - cr % s.R;
+    return s;
+}
 
 template <int NB>
-__global__ void __launch_bounds__(32 * jk32_warps<NB>(), NB > 64 ? 1 : 3) k_jk32(DevBatch b, const int *ctas) {
-    constexpr int WARPS = jk32_warps<NB>();
-    using PL = JKPlan32<NB, WARPS>;
-    constexpr int THREADS = PL::THREADS, LMAX = PL::LMAX, NBUF = PL::NBUF, CR = PL::CR;
-    constexpr int KU = (LMAX / 4 + THREADS - 1) / THREADS;      // 16-byte units per thread
+__global__ void __launch_bounds__(jk32_threads<NB>(), JKPlan32<NB>::CTAS) k_jk32(DevBatch b, const int *ctas) {
+    using PL = JKPlan32<NB>;
+    constexpr int THREADS = PL::THREADS, LMAX = PL::LMAX, AP = PL::AP, RPASS = PL::RPASS, SFL = PL::SFL;
     extern __shared__ __align__(128) unsigned char jsm[];
     uint64_t *bar = (uint64_t *)jsm;
-    float *rho = (float *)(jsm + 128);                          // [NB][NB] swizzled, zero padded
-    double *jq = (double *)(rho + NB * NB);                     // [LMAX] J_Q by ket position
-    double *gred = jq + LMAX;                                   // [THREADS][4]
-    float *stage = (float *)(gred + 4 * THREADS);               // [NBUF][CR * LMAX]
+    float *rho = (float *)(jsm + PL::o_rho);                    // [NB][NB] zero padded
+    double *jq = (double *)(jsm + PL::o_jq);                    // [LMAX] J_Q by (logical) ket position
+    double *corr1 = (double *)(jsm + PL::o_c1), *corr2 = corr1 + NB;
+    float *vps = (float *)(jsm + PL::o_vp);                     // [RPASS] (ij|ij) of the chunk's rows
+    float *stage = (float *)(jsm + PL::o_stage);                // [2][SFL]
     const int cta = ctas[blockIdx.x];
     const int m = b.jk_mol[cta];
     if (b.done[m]) return;
     const int N = b.m_nao[m];
     const int64_t npp = tri(N);
-    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x;
     const float *eri = (const float *)b.eri + b.m_eri0[m];
     const int i0 = b.jk_i0[cta], i1 = b.jk_i1[cta];
+    // chunk producer (thread 0): chunks of consecutive rows of one slab, slabs from i1-1 down to i0
     int pi = i1 - 1, pj = 0;
     auto issue = [&](int slot) {
-        const int nr = min(CR, pi + 1 - pj);
-        const int64_t L = eri_rowlen(pi);
-        bulk_copy(stage + (size_t)slot * CR * LMAX, eri + eri_row(pi, pj), (uint32_t)(nr * L * 4), bar + slot);
-        pj += CR;
+        const JKSlab sp = jk32_slab<NB>(pi);
+        const int nr = min(sp.CR, pi + 1 - pj);
+        // the buffer was last written by generic-proxy stores (in-place partials, scratch)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bulk_copy(stage + (size_t)slot * SFL, eri + eri_row(pi, pj), (uint32_t)(nr * sp.L * 4), bar + slot);
+        pj += sp.CR;
         if (pj > pi) { --pi; pj = 0; }
-        if (JK_PREFETCH > 0) {        // the chunk JK_PREFETCH ahead of the next one, into L2
-            int qi = pi, qj = pj;
-            for (int k = 0; k < JK_PREFETCH && qi >= i0; ++k) {
-                qj += CR;
-                if (qj > qi) { --qi; qj = 0; }
-            }
-            if (qi >= i0) {
-                const int qr = min(CR, qi + 1 - qj);
-                bulk_prefetch_l2(eri + eri_row(qi, qj), (uint32_t)(qr * eri_rowlen(qi) * 4));
-            }
+        if (JK_PREFETCH > 0 && pi >= i0) {       // the chunk after the one just issued, into L2
+            const JKSlab sq = jk32_slab<NB>(pi);
+            const int qr = min(sq.CR, pi + 1 - pj);
+            bulk_prefetch_l2(eri + eri_row(pi, pj), (uint32_t)(qr * sq.L * 4));
         }
     };
     if (tid == 0) {
-        for (int k = 0; k < NBUF; ++k) mbar_init(bar + k, 1);
+        mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int k = 0; k < NBUF && pi >= i0; ++k) issue(k);
+        for (int k = 0; k < 2 && pi >= i0; ++k) issue(k);
     }
     const double *rg = b.rho + b.m_mat0[m];
     for (int t = tid; t < NB * NB; t += THREADS) {
         const int r = t / NB, c = t % NB;
-        rho[rsw32<NB>(r, c)] = (r < N && c < N) ? (float)rg[r * N + c] : 0.f;   // f32-exact in this build
+        rho[t] = (r < N && c < N) ? (float)rg[r * N + c] : 0.f;   // f32-exact in this build
     }
     for (int t = tid; t < LMAX; t += THREADS) jq[t] = 0.0;
     // per-CTA exchange partial (see k_jk)
@@ -482,162 +515,190 @@ __global__ void __launch_bounds__(32 * jk32_warps<NB>(), NB > 64 ? 1 : 3) k_jk32
     int chunk = 0;
     for (int i = i1 - 1; i >= i0; --i) {
         const int A = (i >> 2) + 1;
-        const int S = A <= 1 ? 32 : A <= 2 ? 16 : A <= 4 ? 8 : A <= 8 ? 4 : A <= 16 ? 2 : 1;
-        const int a = lane / S, s = lane % S;
-        const bool lane_ok = a < A;
-        const float *rhoA = rho + 4 * a * NB, *rhoI = rho + i * NB;
-        const int64_t L = eri_rowlen(i);
-        const int units = (int)(L / 4);
-        double gi[4] = {0, 0, 0, 0};
-        float2 jacc[KU][2];                                     // J_Q partials of this slab (f32)
+        const JKSlab sp = jk32_slab<NB>(i);
+        const int nt = sp.nt, L = sp.L, R = sp.R, CR = sp.CR;
+        // reduce pass: PART lanes share the A + 1 terms of one (row, 4-block); a row's lanes span <= 2 warps
+        constexpr int lgAP = AP == 16 ? 4 : 5;
+        const int lgP = 4 * CR * AP <= THREADS ? 2 : 2 * CR * AP <= THREADS ? 1 : 0;
+        const int PART = 1 << lgP;
+        // ---- this thread's tile for the slab
+        const bool mp = tid < R * nt;
+        const int rs = mp ? tid / nt : 0;
+        const int tau = mp ? tid - rs * nt : 0;
+        int ta = (int)((sqrtf(8.f * (float)tau + 1.f) - 1.f) * 0.5f);
+        while (tri32(ta + 1) <= tau) ++ta;
+        while (tri32(ta) > tau) --ta;
+        const int tb = tau - tri32(ta);
+        const int rot = eri_tile_rot(tau);
+        const int o0 = 16 * tau + 4 * (rot & 3), o1 = 16 * tau + 4 * ((rot + 1) & 3);
+        const int o2 = 16 * tau + 4 * ((rot + 2) & 3), o3 = 16 * tau + 4 * ((rot + 3) & 3);
+        const float hs = ta == tb ? 0.5f : 1.f;                 // diagonal tiles: diagonal halved (see k_jk)
+        const float4 rab0 = lds4(rho + (4 * ta) * NB + 4 * tb), rab1 = lds4(rho + (4 * ta + 1) * NB + 4 * tb);
+        const float4 rab2 = lds4(rho + (4 * ta + 2) * NB + 4 * tb), rab3 = lds4(rho + (4 * ta + 3) * NB + 4 * tb);
+        const float4 rib = lds4(rho + i * NB + 4 * tb), ria = lds4(rho + i * NB + 4 * ta);
+        const int tauv0 = tri32(A - 1);                         // tiles of AO i's block row
+        const int ov = 16 * tau + 4 * (((i & 3) + rot) & 3);    // row i & 3 of this tile
+        float2 jqa[4][2];
 #pragma unroll
-        for (int k = 0; k < KU; ++k) jacc[k][0] = jacc[k][1] = make_float2(0.f, 0.f);
+        for (int r = 0; r < 4; ++r) jqa[r][0] = jqa[r][1] = make_float2(0.f, 0.f);
+        double gia[4] = {0, 0, 0, 0}, gib[4] = {0, 0, 0, 0};
+        int slot = 0;
         for (int j0 = 0; j0 <= i; j0 += CR, ++chunk) {
-            const int slot = chunk % NBUF;
-            const float *cbuf = stage + (size_t)slot * CR * LMAX;
-            mbar_wait(bar + slot, (uint32_t)((chunk / NBUF) & 1));
-            const int j = j0 + w;
-            if (w < CR && j <= i) {                             // warp-uniform
-                const float *row = cbuf + (int64_t)w * L;
-                const float *rhoJ = rho + j * NB;
-                double oJ[4] = {0, 0, 0, 0}, oI[4] = {0, 0, 0, 0}, jp = 0.0;
-                if (lane_ok) {
-#pragma unroll kJkQUnr
-                    for (int q = s; q <= A; q += S) {
-                        const bool rp = q <= a;
-                        const int ta = rp ? a : q - 1, tb = rp ? q : a;   // tile (ta, tb)
-                        const int beta = rp ? q : q - 1;                  // rho block of the product
-                        const float *tp = row + 16 * (tri32(ta) + tb);
-                        float tf[16];
-                        {
-                            const float4 r0 = lds4(tp), r1 = lds4(tp + 4), r2 = lds4(tp + 8), r3 = lds4(tp + 12);
-                            tf[0] = r0.x; tf[1] = r0.y; tf[2] = r0.z; tf[3] = r0.w;
-                            tf[4] = r1.x; tf[5] = r1.y; tf[6] = r1.z; tf[7] = r1.w;
-                            tf[8] = r2.x; tf[9] = r2.y; tf[10] = r2.z; tf[11] = r2.w;
-                            tf[12] = r3.x; tf[13] = r3.y; tf[14] = r3.z; tf[15] = r3.w;
-                        }
-                        if (ta == tb) { tf[0] *= 0.5f; tf[5] *= 0.5f; tf[10] *= 0.5f; tf[15] *= 0.5f; }
-                        float t[16];
-#pragma unroll
-                        for (int r = 0; r < 4; ++r)
-#pragma unroll
-                            for (int c = 0; c < 4; ++c) t[4 * r + c] = rp ? tf[4 * r + c] : tf[4 * c + r];
-                        const float4 vj = lds4(rhoJ + ((beta ^ sw32key<NB>(j)) << 2));
-                        const float4 vi = lds4(rhoI + ((beta ^ sw32key<NB>(i)) << 2));
-                        const float2 u[4] = {make_float2(vj.x, vi.x), make_float2(vj.y, vi.y),
-                                             make_float2(vj.z, vi.z), make_float2(vj.w, vi.w)};
-                        // (T rho_j, T rho_i) per result row: one FFMA2 per product pair
-                        float2 o2[4];
-#pragma unroll
-                        for (int r = 0; r < 4; ++r) {
-                            float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-                            for (int c = 0; c < 4; ++c)
-                                acc = __ffma2_rn(make_float2(t[4 * r + c], t[4 * r + c]), u[c], acc);
-                            o2[r] = acc;
-                        }
-#pragma unroll
-                        for (int r = 0; r < 4; ++r) {
-                            oJ[r] += (double)o2[r].x;
-                            oI[r] += (double)o2[r].y;
-                        }
-                        if (rp) {                               // J_P: row-part tiles only
-                            const int key = sw32key<NB>(4 * a);
-                            float2 d2 = make_float2(0.f, 0.f);
-#pragma unroll
-                            for (int r = 0; r < 4; ++r) {
-                                const float4 x = lds4(rhoA + r * NB + ((beta ^ key) << 2));
-                                d2 = __ffma2_rn(make_float2(t[4 * r], t[4 * r + 1]), make_float2(x.x, x.y), d2);
-                                d2 = __ffma2_rn(make_float2(t[4 * r + 2], t[4 * r + 3]), make_float2(x.z, x.w), d2);
-                            }
-                            jp += (double)d2.x + (double)d2.y;
-                        }
+            slot = chunk & 1;
+            float *cbuf = stage + (size_t)slot * SFL;
+            mbar_wait(bar + slot, (uint32_t)((chunk >> 1) & 1));
+            const int nr = min(CR, i + 1 - j0);
+            if (mp) {
+                for (int rr = rs; rr < nr; rr += R) {
+                    const int j = j0 + rr;
+                    float *tp = cbuf + rr * L;
+                    float4 T0 = lds4(tp + o0), T1 = lds4(tp + o1), T2 = lds4(tp + o2), T3 = lds4(tp + o3);
+                    if (tau == tauv0 + (j >> 2)) vps[rr] = tp[ov + (j & 3)];      // (ij|ij)
+                    const float *rj = rho + j * NB;
+                    const float4 rjb = lds4(rj + 4 * tb), rja = lds4(rj + 4 * ta);
+                    const float2 w2 = dup2(rho[i * NB + j] * (i != j ? 2.f : 1.f));   // exact
+                    // J_Q += v_PQ rho~_P on the stored values
+                    jqa[0][0] = __ffma2_rn(lo2(T0), w2, jqa[0][0]); jqa[0][1] = __ffma2_rn(hi2(T0), w2, jqa[0][1]);
+                    jqa[1][0] = __ffma2_rn(lo2(T1), w2, jqa[1][0]); jqa[1][1] = __ffma2_rn(hi2(T1), w2, jqa[1][1]);
+                    jqa[2][0] = __ffma2_rn(lo2(T2), w2, jqa[2][0]); jqa[2][1] = __ffma2_rn(hi2(T2), w2, jqa[2][1]);
+                    jqa[3][0] = __ffma2_rn(lo2(T3), w2, jqa[3][0]); jqa[3][1] = __ffma2_rn(hi2(T3), w2, jqa[3][1]);
+                    T0.x *= hs; T1.y *= hs; T2.z *= hs; T3.w *= hs;
+                    // row part (result block ta): T rho_j[tb] -> G_i, T rho_i[tb] -> G_j
+                    const float oJ0 = dot4(T0, rjb), oJ1 = dot4(T1, rjb), oJ2 = dot4(T2, rjb), oJ3 = dot4(T3, rjb);
+                    const float4 oI = make_float4(dot4(T0, rib), dot4(T1, rib), dot4(T2, rib), dot4(T3, rib));
+                    // column part (result block tb): T^T rho_j[ta] -> G_i, T^T rho_i[ta] -> G_j
+                    float2 cJ0 = __ffma2_rn(lo2(T0), dup2(rja.x), make_float2(0.f, 0.f));
+                    float2 cJ1 = __ffma2_rn(hi2(T0), dup2(rja.x), make_float2(0.f, 0.f));
+                    float2 cI0 = __ffma2_rn(lo2(T0), dup2(ria.x), make_float2(0.f, 0.f));
+                    float2 cI1 = __ffma2_rn(hi2(T0), dup2(ria.x), make_float2(0.f, 0.f));
+                    cJ0 = __ffma2_rn(lo2(T1), dup2(rja.y), cJ0); cJ1 = __ffma2_rn(hi2(T1), dup2(rja.y), cJ1);
+                    cI0 = __ffma2_rn(lo2(T1), dup2(ria.y), cI0); cI1 = __ffma2_rn(hi2(T1), dup2(ria.y), cI1);
+                    cJ0 = __ffma2_rn(lo2(T2), dup2(rja.z), cJ0); cJ1 = __ffma2_rn(hi2(T2), dup2(rja.z), cJ1);
+                    cI0 = __ffma2_rn(lo2(T2), dup2(ria.z), cI0); cI1 = __ffma2_rn(hi2(T2), dup2(ria.z), cI1);
+                    cJ0 = __ffma2_rn(lo2(T3), dup2(rja.w), cJ0); cJ1 = __ffma2_rn(hi2(T3), dup2(rja.w), cJ1);
+                    cI0 = __ffma2_rn(lo2(T3), dup2(ria.w), cI0); cI1 = __ffma2_rn(hi2(T3), dup2(ria.w), cI1);
+                    // J_P term of this tile: sum T . rho[ta-block][tb-block] (two f32 partials)
+                    float2 jp2 = __ffma2_rn(lo2(T0), lo2(rab0), make_float2(0.f, 0.f));
+                    jp2 = __ffma2_rn(hi2(T0), hi2(rab0), jp2);
+                    jp2 = __ffma2_rn(lo2(T1), lo2(rab1), jp2); jp2 = __ffma2_rn(hi2(T1), hi2(rab1), jp2);
+                    jp2 = __ffma2_rn(lo2(T2), lo2(rab2), jp2); jp2 = __ffma2_rn(hi2(T2), hi2(rab2), jp2);
+                    jp2 = __ffma2_rn(lo2(T3), lo2(rab3), jp2); jp2 = __ffma2_rn(hi2(T3), hi2(rab3), jp2);
+                    gia[0] += (double)oJ0; gia[1] += (double)oJ1; gia[2] += (double)oJ2; gia[3] += (double)oJ3;
+                    gib[0] += (double)cJ0.x; gib[1] += (double)cJ0.y; gib[2] += (double)cJ1.x; gib[3] += (double)cJ1.y;
+                    // G_j and J_P terms over the consumed tile: slot 0 row part, 1 column part, 2 J_P
+                    *reinterpret_cast<float4 *>(tp + o0) = oI;
+                    *reinterpret_cast<float4 *>(tp + o1) = make_float4(cI0.x, cI0.y, cI1.x, cI1.y);
+                    *reinterpret_cast<float2 *>(tp + o2) = jp2;
+                }
+            }
+            __syncthreads();
+            {   // ---- reduce pass: G_j = 2 sum of the A + 1 tile terms of each (row, 4-block)
+                const int rr = tid >> (lgAP + lgP), a = (tid >> lgP) & (AP - 1), part = tid & (PART - 1);
+                const bool act = rr < nr && a < A;
+                float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;   // this lane's terms (f32), then f64 across the lanes
+                if (act) {
+                    const float *rp = cbuf + rr * L;
+                    int k = part;
+                    for (int tq = tri32(a) + k; k <= a; k += PART, tq += PART) {   // row part: tiles (a, k), slot 0
+                        const float4 v = lds4(rp + 16 * tq + 4 * eri_tile_rot(tq));
+                        s0 += v.x; s1 += v.y; s2 += v.z; s3 += v.w;
+                    }
+                    for (; k <= A; k += PART) {                                    // column part: tiles (k - 1, a), slot 1
+                        const int tq = tri32(k - 1) + a;
+                        const float4 v = lds4(rp + 16 * tq + 4 * ((eri_tile_rot(tq) + 1) & 3));
+                        s0 += v.x; s1 += v.y; s2 += v.z; s3 += v.w;
                     }
                 }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) gi[u] = fma(2.0, oJ[u], gi[u]);
-                for (int o = 1; o < S; o <<= 1)
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) oI[u] += shfl_x(oI[u], o);
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) jp += shfl_x(jp, o);
-                const double vp = (double)row[eri_ket(i, j)];
-                const double rjI = rho[rsw32<NB>(j, i)], rjJ = rho[rsw32<NB>(j, j)];
-                const double riI = rho[rsw32<NB>(i, i)], riJ = rho[rsw32<NB>(i, j)];
-                if (lane_ok && s == 0) {
+                double d0 = (double)s0, d1 = (double)s1, d2 = (double)s2, d3 = (double)s3;
+                for (int o = 1; o < PART; o <<= 1) {
+                    d0 += shfl_x(d0, o); d1 += shfl_x(d1, o); d2 += shfl_x(d2, o); d3 += shfl_x(d3, o);
+                }
+                if (act && part == 0) {
+                    const int j = j0 + rr;
+                    const double vp = (double)vps[rr];
+                    const double riI = rho[i * NB + i], riJ = rho[i * NB + j];
+                    const double g[4] = {2.0 * d0, 2.0 * d1, 2.0 * d2, 2.0 * d3};
                     double *Gj = Gp + (int64_t)j * N;
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         const int t = 4 * a + u;
-                        double gJ = 2.0 * oI[u];
-                        if (t == j) { gi[u] -= vp * rjI; gJ -= vp * riI; }
-                        else if (t == i) { gi[u] -= vp * rjJ; gJ -= vp * riJ; }
-                        if (j < i && t <= i) atomicAdd(Gj + t, gJ);   // RED, order fixed by the chunk barriers
+                        double gJ = g[u];
+                        if (t == j) gJ -= vp * riI;
+                        else if (t == i) gJ -= vp * riJ;
+                        if (j < i && t <= i) atomicAdd(Gj + t, gJ);   // RED; one add per element per chunk
+                    }
+                    if (a == (j >> 2)) {                           // this row's corrections to G_i (applied at slab end)
+                        corr1[j] = vp * (double)rho[j * NB + i];
+                        corr2[j] = j < i ? vp * (double)rho[j * NB + j] : 0.0;
                     }
                 }
-                if (lane == 0) Jp[tri(i) + j] = 2.0 * jp - vp * riJ * (i != j ? 2.0 : 1.0);
-            }
-            // ---- J_Q += v_PQ rho~_P over the chunk's rows (thread-owned 16-byte units, f32)
-            const int nr = min(CR, i + 1 - j0);
-            for (int rr = 0; rr < nr; ++rr) {
-                const int jj = j0 + rr;
-                const float wgt = rho[rsw32<NB>(i, jj)] * (i != jj ? 2.f : 1.f);   // exact
-                const float2 w2 = make_float2(wgt, wgt);
-                const float *rowp = cbuf + (int64_t)rr * L;
-#pragma unroll
-                for (int k = 0; k < KU; ++k) {
-                    const int u = tid + k * THREADS;
-                    if (u < units) {
-                        const float4 v = lds4(rowp + 4 * u);
-                        jacc[k][0] = __ffma2_rn(make_float2(v.x, v.y), w2, jacc[k][0]);
-                        jacc[k][1] = __ffma2_rn(make_float2(v.z, v.w), w2, jacc[k][1]);
+                // ---- J_P = 2 sum of the row's tile terms - the (ij|ij) image counted by J_Q: one warp per row
+                for (int r2 = tid >> 5; r2 < nr; r2 += THREADS / 32) {
+                    const float *rp = cbuf + r2 * L;
+                    double jp = 0.0;
+                    for (int tq = tid & 31; tq < nt; tq += 32) {
+                        const float2 q = *reinterpret_cast<const float2 *>(rp + 16 * tq + 4 * ((eri_tile_rot(tq) + 2) & 3));
+                        jp += (double)q.x + (double)q.y;
+                    }
+                    jp = warp_sum(jp);
+                    if ((tid & 31) == 0) {
+                        const int j = j0 + r2;
+                        const double vp = (double)vps[r2], riJ = rho[i * NB + j];
+                        Jp[tri(i) + j] = 2.0 * jp - vp * riJ * (i != j ? 2.0 : 1.0);
                     }
                 }
             }
-            __syncthreads();                           // chunk consumed
-            if (tid == 0 && pi >= i0) issue(slot);
+            __syncthreads();
+            // refill the consumed buffer; the slab's last chunk is refilled after the slab-end reductions
+            if (tid == 0 && pi >= i0 && j0 + CR <= i) issue(slot);
         }
-        // ---- slab end: J_Q partials into the f64 accumulators; G_i fixed-order sums
+        // ---- slab end: J_Q and G_i reduced over the row groups / tiles through the free stage buffer
+        float *scr = stage + (size_t)slot * SFL;
+        if (mp) {
+            float *q = scr + (rs * nt + tau) * 16;
 #pragma unroll
-        for (int k = 0; k < KU; ++k) {
-            const int u = tid + k * THREADS;
-            if (u < units) {
-                double2 *q2 = reinterpret_cast<double2 *>(jq + 4 * u);
-                double2 x = q2[0], y = q2[1];
-                x.x += (double)jacc[k][0].x; x.y += (double)jacc[k][0].y;
-                y.x += (double)jacc[k][1].x; y.y += (double)jacc[k][1].y;
-                q2[0] = x;
-                q2[1] = y;
-            }
-        }
-        for (int o = 1; o < S; o <<= 1)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) gi[u] += shfl_x(gi[u], o);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) gred[tid * 4 + u] = gi[u];
-        __syncthreads();
-        if (tid < A) {                                 // thread tid handles block tid
-            double *Gi = Gp + (int64_t)i * N;
-            for (int u = 0; u < 4; ++u) {
-                const int t = 4 * tid + u;
-                if (t > i) break;
-                double v = 0.0;
-                for (int ww = 0; ww < CR; ++ww) v += gred[(ww * 32 + tid * S) * 4 + u];
-                atomicAdd(Gi + t, v);
-            }
+            for (int r = 0; r < 4; ++r)
+                *reinterpret_cast<float4 *>(q + 4 * r) = make_float4(jqa[r][0].x, jqa[r][0].y, jqa[r][1].x, jqa[r][1].y);
         }
         __syncthreads();
+        for (int e = tid; e < L; e += THREADS) {
+            double s = jq[e];
+            for (int g = 0; g < R; ++g) s += (double)scr[g * L + e];
+            jq[e] = s;
+        }
+        __syncthreads();
+        double *sd = reinterpret_cast<double *>(scr);
+        if (mp) {
+            double2 *q = reinterpret_cast<double2 *>(sd + (rs * nt + tau) * 8);
+            q[0] = make_double2(gia[0], gia[1]); q[1] = make_double2(gia[2], gia[3]);
+            q[2] = make_double2(gib[0], gib[1]); q[3] = make_double2(gib[2], gib[3]);
+        }
+        __syncthreads();
+        if (tid <= i) {                                        // G_i[t], t = tid
+            const int a = tid >> 2, u = tid & 3, ra = tri32(a);
+            double s = 0.0;
+            for (int g = 0; g < R; ++g) {
+                const double *q = sd + (size_t)g * nt * 8;
+                for (int k = 0; k <= A; ++k) s += k <= a ? q[(ra + k) * 8 + u] : q[(tri32(k - 1) + a) * 8 + 4 + u];
+            }
+            double gv = 2.0 * s - corr1[tid];
+            if (tid == i)
+                for (int j = 0; j < i; ++j) gv -= corr2[j];
+            atomicAdd(Gp + (int64_t)i * N + tid, gv);
+        }
+        __syncthreads();
+        if (tid == 0 && pi >= i0) issue(slot);
     }
     // ---- this CTA's J_Q partial, every Q of the molecule written once
     const int local = cta - b.m_jkcta0[m];
     double *Js = Jp + (int64_t)(1 + local) * npp;
-    const int64_t Lm = eri_rowlen(N - 1);
+    const int Lm = (int)eri_rowlen(N - 1);
     for (int e = tid; e < Lm; e += THREADS) {
         const int tau = e >> 4;
-        int a = (int)((sqrt(8.0 * (double)tau + 1.0) - 1.0) * 0.5);
-        while (tri(a + 1) <= tau) ++a;
-        while (tri(a) > tau) --a;
-        const int bb = tau - (int)tri(a);
+        int a = (int)((sqrtf(8.f * (float)tau + 1.f) - 1.f) * 0.5f);
+        while (tri32(a + 1) <= tau) ++a;
+        while (tri32(a) > tau) --a;
+        const int bb = tau - tri32(a);
         const int kk = 4 * a + ((e >> 2) & 3), ll = 4 * bb + (e & 3);
         if (kk < N && ll <= kk) Js[tri(kk) + ll] = jq[e];
     }
@@ -645,7 +706,7 @@ __global__ void __launch_bounds__(32 * jk32_warps<NB>(), NB > 64 ? 1 : 3) k_jk32
 
 template <int NB>
 static void launch_bucket32(const DevBatch &b, const int *ctas, int n, cudaStream_t s) {
-    using PL = JKPlan32<NB, jk32_warps<NB>()>;
+    using PL = JKPlan32<NB>;
     smem_optin((const void *)k_jk32<NB>);
     k_jk32<NB><<<n, PL::THREADS, PL::bytes, s>>>(b, ctas);
 }
@@ -676,9 +737,8 @@ static void launch_jk_t(const DevBatch &b, const int *bucket_ctas, const int *bu
 // bucket_ctas: device array of CTA indices grouped by AO-count bucket; bucket_n: host counts [6]
 int launch_jk(const DevBatch &b, const int *bucket_ctas, const int *bucket_n, cudaStream_t s) {
     if (b.n_jk_cta == 0) return 0;
-    if (b.eri64 || !JK32) {
-        if (b.eri64) launch_jk_t<double>(b, bucket_ctas, bucket_n, s);
-        else launch_jk_t<float>(b, bucket_ctas, bucket_n, s);
+    if (b.eri64) {
+        launch_jk_t<double>(b, bucket_ctas, bucket_n, s);
     } else {
         const int *c = bucket_ctas;
         if (bucket_n[0]) launch_bucket32<16>(b, c, bucket_n[0], s);
