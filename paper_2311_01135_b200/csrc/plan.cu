@@ -59,7 +59,18 @@ static int fail(int code, const std::string &msg) {
     } while (0)
 
 static constexpr int XC_CHUNK = 2048;
-static constexpr int JK_SPLIT = 12;
+// Target J/K CTAs per molecule (largest slab permitting).  A CTA's fixed costs (density load,
+// zeroing and later summing its N x N exchange partial, J_Q flush, pipeline fill) favour few,
+// long CTAs once the batch alone fills the GPU: measured on B200 with 256 molecules x 9 heavy
+// atoms, J/K per iteration 1.05 ms at 12, 0.97 at 8, 0.95 at 4, 0.94 at 3 (296 resident CTAs).
+// Small batches keep more CTAs per molecule so a single molecule still spreads over the SMs.
+// QM1B_JK_SPLIT overrides (tuning runs).
+static int jk_split(int n_mol) {
+    static const int env = [] { const char *e = getenv("QM1B_JK_SPLIT"); return e ? atoi(e) : 0; }();
+    if (env > 0) return env;
+    const int per = (600 + n_mol - 1) / std::max(1, n_mol);
+    return std::max(4, std::min(16, per));
+}
 #ifndef ERI64_F32
 #define ERI64_F32 0     // f32 build: keep the (f32-rounded) ERI store in f64 (no f32->f64 in J/K)
 #endif     // target J/K CTAs per molecule (largest slab permitting)
@@ -368,7 +379,7 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
                 tot += wk[i];
                 wmax = std::max(wmax, wk[i]);
             }
-            const int64_t target = std::max(wmax, (tot + JK_SPLIT - 1) / JK_SPLIT);
+            const int64_t target = std::max(wmax, (tot + jk_split(nm) - 1) / jk_split(nm));
             int hi = (int)N;
             int64_t acc = 0;
             for (int i = (int)N - 1; i >= 0; --i) {
