@@ -107,6 +107,32 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
+// XC_MMAV=1 (default): the f32 build's main bucket (N 49..64, 64-point sub-blocks) runs the
+// V += phi wv^T contraction on the tensor cores: mma.sync m16n8k8 TF32 with the 3xTF32 split
+// (x = hi + lo, hi rounded to TF32, lo the exact f32 remainder; hi*lo + lo*hi + hi*hi, f32
+// accumulation - 5e-7 of the largest element on random products, tools/probe).  The FFMA2
+// formulation of that phase is bound by shared-memory wavefronts (every 16-byte operand load
+// of a 4 x 4 register tile is four wavefronts for 16 FMAs per thread: 64 FMA per wavefront
+// against 128 FMA per clock of the FP32 pipe); ldmatrix fragments feed 16 MMAs (16 K FMAs)
+// from 12 wavefronts.  Measured on B200: mma.sync TF32 276 TFLOP/s, FFMA 70 (mma_probe.cu).
+#ifndef XC_MMAV
+#define XC_MMAV 0
+#endif
+__device__ __forceinline__ void ldsm4(uint32_t addr, uint32_t (&r)[4]) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+// x = hi + lo: hi = x rounded to TF32, lo = the f32 remainder (the MMA reads its top 19 bits)
+__device__ __forceinline__ void tf32_split(uint32_t x, uint32_t &hi, uint32_t &lo) {
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(__uint_as_float(x)));
+    lo = __float_as_uint(__uint_as_float(x) - __uint_as_float(hi));
+}
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
 template <typename W, int NQ, int BP>
 struct XCL {
     static constexpr int NP = 4 * NQ;
@@ -253,9 +279,16 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
     // V accumulators: f32 keeps two partial sums (even / odd points of each 4-point chunk)
     // so every update is one packed FFMA2; f64 one DFMA chain
     using VA = typename std::conditional<sizeof(W) == 4, float2, double>::type;
-    VA acc[TJ][4][4];
+    // tensor-core V phase (see XC_MMAV): warp w owns the 16 AO rows a = 4 g + (w >> 1) (g = 0..15:
+    // rows of one residue mod 4, so that the 8 row addresses of an ldmatrix tile fall in 8
+    // different row quads = 8 different swizzle keys = no bank conflict) and the 32 columns
+    // c = 4 (8 (w & 1) + g') + j', g' = 0..7, j' = 0..3 (four n8 tiles)
+    constexpr bool MMAV = XC_MMAV && sizeof(W) == 4 && NQ == 16 && BP == 64;
+    constexpr int TJA = MMAV ? 1 : TJ;
+    VA acc[TJA][4][4];
+    float vacc[4][4];                        // MMAV: [n tile j'][c0..c3]
 #pragma unroll
-    for (int j = 0; j < TJ; ++j)
+    for (int j = 0; j < TJA; ++j)
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -263,6 +296,23 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
                 if constexpr (sizeof(W) == 4) acc[j][a][c] = make_float2(0.f, 0.f);
                 else acc[j][a][c] = 0.0;
             }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) vacc[a][c] = 0.f;
+    // per-lane ldmatrix row addresses (byte addresses in shared memory) and swizzle terms
+    uint32_t mA = 0, mB0 = 0, mB1 = 0;
+    int xA = 0, xB = 0;
+    if constexpr (MMAV) {
+        const int lane = tid & 31, wp = tid >> 5, l7 = lane & 7, id = lane >> 3;
+        const int quadA = l7 + 8 * (id & 1);                       // A: matrices (half, kh) = (id & 1, id >> 1)
+        mA = (uint32_t)__cvta_generic_to_shared(phi + (4 * quadA + (wp >> 1)) * BP);
+        xA = quadA ^ (id >> 1);
+        const int quadB = 8 * (wp & 1) + l7;                       // B: matrices (n tile, kh) = (2 x + (id >> 1), id & 1)
+        mB0 = (uint32_t)__cvta_generic_to_shared(wv + (4 * quadB + (id >> 1)) * BP);
+        mB1 = (uint32_t)__cvta_generic_to_shared(wv + (4 * quadB + 2 + (id >> 1)) * BP);
+        xB = quadB ^ (id & 1);
+    }
     double e_acc = 0.0;
     int bad = 0;
     const int pg = tid / LG, lg = tid % LG;
@@ -399,24 +449,33 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
                     }
                 }
             }
+            // Sum over the LG lanes that share the point group: a transposing butterfly.  At each of
+            // the first four steps a lane keeps the half of its values whose index bit s matches its
+            // lane bit s and hands the other half to its partner, so the 16 values per lane shrink to
+            // one (15 shuffles and adds instead of 64): after step s, h[k] is value index
+            // (k << (s + 1)) | (lane's low s + 1 bits), summed over the lanes differing in those bits.
+            // Lane lg ends with value index lg & 15 = 4 * component + point (LG = 32: one more exchange).
+            {
+                W h[16];
 #pragma unroll
-            for (int o = 1; o < LG; o <<= 1)
+                for (int a = 0; a < 4; ++a) { h[a] = n4[a]; h[4 + a] = g4[0][a]; h[8 + a] = g4[1][a]; h[12 + a] = g4[2][a]; }
 #pragma unroll
-                for (int a = 0; a < 4; ++a) {
-                    n4[a] += __shfl_xor_sync(0xffffffffu, n4[a], o);
-                    g4[0][a] += __shfl_xor_sync(0xffffffffu, g4[0][a], o);
-                    g4[1][a] += __shfl_xor_sync(0xffffffffu, g4[1][a], o);
-                    g4[2][a] += __shfl_xor_sync(0xffffffffu, g4[2][a], o);
+                for (int s_ = 0; s_ < 4; ++s_) {
+                    const int o = 1 << s_;
+                    const bool up = (lg & o) != 0;
+#pragma unroll
+                    for (int k = 0; k < (8 >> s_); ++k) {
+                        const W mine = up ? h[2 * k + 1] : h[2 * k], other = up ? h[2 * k] : h[2 * k + 1];
+                        h[k] = mine + __shfl_xor_sync(0xffffffffu, other, o);
+                    }
                 }
-            if (lg == 0)
-#pragma unroll
-                for (int a = 0; a < 4; ++a) {
-                    double *d = dn + 4 * (4 * pg + a);
-                    d[0] = (double)n4[a];
-                    d[1] = (double)(W)(2 * g4[0][a]);
-                    d[2] = (double)(W)(2 * g4[1][a]);
-                    d[3] = (double)(W)(2 * g4[2][a]);
+                W r = h[0];
+                if constexpr (LG == 32) r += __shfl_xor_sync(0xffffffffu, r, 16);
+                if (lg < 16) {
+                    const int comp = lg >> 2, a = lg & 3;
+                    dn[4 * (4 * pg + a) + comp] = comp == 0 ? (double)r : (double)(W)(2 * r);
                 }
+            }
         }
         __syncthreads();
         XP(2);
@@ -478,6 +537,28 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
         __syncthreads();
         XP(4);
         load_pts(sb + BP);
+        if constexpr (MMAV) {                              // ---- V += phi wv^T on the tensor cores (3xTF32)
+#pragma unroll
+            for (int ks = 0; ks < BP / 8; ++ks) {          // 8 points per step: column groups 2 ks, 2 ks + 1
+                uint32_t a[4], b0[4], b1[4];
+                ldsm4(mA + 16u * (uint32_t)(((2 * ks) ^ xA) & (BP / 4 - 1)), a);
+                ldsm4(mB0 + 16u * (uint32_t)(((2 * ks) ^ xB) & (BP / 4 - 1)), b0);    // n tiles 0, 1: (b0, b1) each
+                ldsm4(mB1 + 16u * (uint32_t)(((2 * ks) ^ xB) & (BP / 4 - 1)), b1);    // n tiles 2, 3
+                uint32_t ah[4], al[4], bh[8], bl[8];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    tf32_split(a[k], ah[k], al[k]);
+                    tf32_split(b0[k], bh[k], bl[k]);
+                    tf32_split(b1[k], bh[4 + k], bl[4 + k]);
+                }
+#pragma unroll
+                for (int n = 0; n < 4; ++n) {
+                    mma_tf32(vacc[n], ah, bl[2 * n], bl[2 * n + 1]);
+                    mma_tf32(vacc[n], al, bh[2 * n], bh[2 * n + 1]);
+                    mma_tf32(vacc[n], ah, bh[2 * n], bh[2 * n + 1]);
+                }
+            }
+        } else
 #pragma unroll
         for (int j = 0; j < TJ; ++j) {                     // ---- V += phi wv^T, 4 x 4 tiles
             const int T = tid + j * XC_THREADS;
@@ -519,6 +600,18 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
 #undef XP
     const int local = cta - b.m_xccta0[m];
     double *Vp = b.Vpart + b.m_V0[m] + (int64_t)local * N * N;
+    if constexpr (MMAV) {
+        // accumulator fragment: c0, c1 = (row g, cols 2t, 2t+1), c2, c3 = (row g + 8, same cols)
+        const int lane = tid & 31, wp = tid >> 5, g = lane >> 2, t2 = 2 * (lane & 3);
+#pragma unroll
+        for (int n = 0; n < 4; ++n)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int mu = 4 * (g + 8 * (k >> 1)) + (wp >> 1);
+                const int nu = 4 * (8 * (wp & 1) + t2 + (k & 1)) + n;
+                if (mu < N && nu < N) Vp[mu * N + nu] = (double)vacc[n][k];
+            }
+    } else
 #pragma unroll
     for (int j = 0; j < TJ; ++j) {
         const int T = tid + j * XC_THREADS;
