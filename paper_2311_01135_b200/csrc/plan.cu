@@ -65,9 +65,10 @@ static constexpr int XC_CHUNK = 2048;
 // atoms, J/K per iteration 1.05 ms at 12, 0.97 at 8, 0.95 at 4, 0.94 at 3 (296 resident CTAs).
 // Small batches keep more CTAs per molecule so a single molecule still spreads over the SMs.
 // QM1B_JK_SPLIT overrides (tuning runs).
-static int jk_split(int n_mol) {
+static int jk_split(int n_mol, int f32_store) {
     static const int env = [] { const char *e = getenv("QM1B_JK_SPLIT"); return e ? atoi(e) : 0; }();
     if (env > 0) return env;
+    if (!f32_store) return 12;                 // f64 store: k_jk (one warp per row, 4-8 warps per CTA) as tuned in round 1
     const int per = (600 + n_mol - 1) / std::max(1, n_mol);
     return std::max(4, std::min(16, per));
 }
@@ -379,7 +380,8 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
                 tot += wk[i];
                 wmax = std::max(wmax, wk[i]);
             }
-            const int64_t target = std::max(wmax, (tot + jk_split(nm) - 1) / jk_split(nm));
+            const int js = jk_split(nm, opts->precision && !ERI64_F32);
+            const int64_t target = std::max(wmax, (tot + js - 1) / js);
             int hi = (int)N;
             int64_t acc = 0;
             for (int i = (int)N - 1; i >= 0; --i) {
