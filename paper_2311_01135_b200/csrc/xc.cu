@@ -538,6 +538,14 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
         XP(4);
         load_pts(sb + BP);
         if constexpr (MMAV) {                              // ---- V += phi wv^T on the tensor cores (3xTF32)
+            // the MMA accumulates one sub-block (64 points) from zero; the CTA-lifetime sums are
+            // round-to-nearest adds (the tensor core's own f32 accumulation truncates: over the
+            // CTA's 2048 points that bias tripled the V_xc error)
+            float sacc[4][4];
+#pragma unroll
+            for (int n = 0; n < 4; ++n)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) sacc[n][k] = 0.f;
 #pragma unroll
             for (int ks = 0; ks < BP / 8; ++ks) {          // 8 points per step: column groups 2 ks, 2 ks + 1
                 uint32_t a[4], b0[4], b1[4];
@@ -553,11 +561,15 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
                 }
 #pragma unroll
                 for (int n = 0; n < 4; ++n) {
-                    mma_tf32(vacc[n], ah, bl[2 * n], bl[2 * n + 1]);
-                    mma_tf32(vacc[n], al, bh[2 * n], bh[2 * n + 1]);
-                    mma_tf32(vacc[n], ah, bh[2 * n], bh[2 * n + 1]);
+                    mma_tf32(sacc[n], ah, bl[2 * n], bl[2 * n + 1]);
+                    mma_tf32(sacc[n], al, bh[2 * n], bh[2 * n + 1]);
+                    mma_tf32(sacc[n], ah, bh[2 * n], bh[2 * n + 1]);
                 }
             }
+#pragma unroll
+            for (int n = 0; n < 4; ++n)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) vacc[n][k] += sacc[n][k];
         } else
 #pragma unroll
         for (int j = 0; j < TJ; ++j) {                     // ---- V += phi wv^T, 4 x 4 tiles
