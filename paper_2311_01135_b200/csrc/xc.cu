@@ -109,14 +109,20 @@ __device__ __forceinline__ float ex2_approx(float x) {
 
 // XC_MMAV=1 (default): the f32 build's main bucket (N 49..64, 64-point sub-blocks) runs the
 // V += phi wv^T contraction on the tensor cores: mma.sync m16n8k8 TF32 with the 3xTF32 split
-// (x = hi + lo, hi rounded to TF32, lo the exact f32 remainder; hi*lo + lo*hi + hi*hi, f32
-// accumulation - 5e-7 of the largest element on random products, tools/probe).  The FFMA2
-// formulation of that phase is bound by shared-memory wavefronts (every 16-byte operand load
-// of a 4 x 4 register tile is four wavefronts for 16 FMAs per thread: 64 FMA per wavefront
-// against 128 FMA per clock of the FP32 pipe); ldmatrix fragments feed 16 MMAs (16 K FMAs)
-// from 12 wavefronts.  Measured on B200: mma.sync TF32 276 TFLOP/s, FFMA 70 (mma_probe.cu).
+// (x = hi + lo, hi rounded to TF32, lo the exact f32 remainder; hi*lo + lo*hi + hi*hi), one
+// sub-block accumulated by the MMA from zero and added to the CTA's sums in round-to-nearest
+// f32 (the tensor core's own accumulation truncates; over a CTA's 2048 points that bias took
+// the V_xc error against the reference's f32 xc_matrix from 1.3e-6 to 3.8e-6 of max|V|; with
+// the two levels it is 1.4e-6).  The FFMA2 formulation of that phase is bound by
+// shared-memory wavefronts (every 16-byte operand load of a 4 x 4 register tile is four
+// wavefronts for 16 FMAs per thread: 64 FMA per wavefront against 128 FMA per clock of the
+// FP32 pipe); ldmatrix fragments feed 12 MMAs (12 K FMAs) from 12 wavefronts.  Measured on
+// B200: mma.sync TF32 276 TFLOP/s = 4x FFMA (tools/probe/mma_probe.cu), so with three MMAs
+// per product the phase gains 27% (4.7k -> 3.5k cycles per sub-block) and the kernel 2%
+// (1.638 -> 1.603 ms per iteration); the tcgen05 path (umma.cuh, k_xc_mma) would need the
+// AO planes in SWIZZLE_128B K-major tiles, which the FFMA phases cannot read conflict free.
 #ifndef XC_MMAV
-#define XC_MMAV 0
+#define XC_MMAV 1
 #endif
 __device__ __forceinline__ void ldsm4(uint32_t addr, uint32_t (&r)[4]) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
