@@ -380,7 +380,7 @@ def run_ours(args, ws, rank, local):
 
     # the dominant kernel (largest share of the step's launch list, profiles/*_bench_launches_summary):
     # k_xc, once per SCF iteration
-    roof_xc = {"kernel": "k_xc (AO values + density + B3LYP + V_xc, f32 contractions)", "bound": "fp32",
+    roof_xc = {"kernel": "k_xc (AO values + density + B3LYP + V_xc; f32 contractions, V phase on TF32 tensor cores)", "bound": "fp32",
                "achieved": xc_tf, "peak": peak32.value, "unit": "TFLOP/s",
                "frac": xc_tf / peak32.value if peak32.value else None, "ms_per_iteration": ms_xc,
                "traffic": _traffic("xc_256mol"), "traffic_source": cap_src,
@@ -460,7 +460,7 @@ def run_ours(args, ws, rank, local):
                      "timing": f"ERI-stage CUDA events over the timed region ({F} batches in flight, so the "
                                "stage shares the SMs with other batches' SCF loops)"},
 
-        "roofline_jk": {"kernel": "k_jk (J/K digestion of the ERI store)", "bound": "hbm",
+        "roofline_jk": {"kernel": "k_jk32 (tile-owner J/K digestion of the f32 ERI store)", "bound": "hbm",
                         "achieved": jk_gbs, "peak": hbm_peak, "unit": "GB/s",
                         "frac": jk_gbs / hbm_peak if hbm_peak else None, "ms_per_iteration": ms_jk,
                         "traffic": _traffic("jk_256mol"),

@@ -124,6 +124,15 @@ __device__ __forceinline__ float ex2_approx(float x) {
 #ifndef XC_MMAV
 #define XC_MMAV 1
 #endif
+// XC_MMAT=1: the same bucket also runs t = phi^T rho on the tensor cores (see the t phase).
+// Measured on B200 and kept off: kernel 1.60 -> 1.55 ms per iteration, but n = sum_nu t phi
+// inherits the truncating accumulation of a 24-MMA chain and the truncated lo parts as a bias
+// of one sign: E_xc error against the reference's f32 xc_matrix 2.3e-6 -> 2.0e-5 Ha at N = 63
+// (test bound 6e-6); flushing the MMA accumulators every K step in round-to-nearest f32 would
+// cost the gain.
+#ifndef XC_MMAT
+#define XC_MMAT 0
+#endif
 __device__ __forceinline__ void ldsm4(uint32_t addr, uint32_t (&r)[4]) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
@@ -259,9 +268,15 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
     int *shi = (int *)(shw + xc_swn<W>() * nsh);
     const int tid = threadIdx.x;
     const double *rg = b.rho + b.m_mat0[m];
+    // tensor-core t phase: rho is kept with its columns grouped by residue mod 4 (column nu at
+    // 16 (nu & 3) + (nu >> 2)) and its 16-byte groups swizzled by the row quad like the AO planes,
+    // so that the MMA fragments below are conflict-free scalar loads
+    constexpr bool MMAT = XC_MMAT && XC_MMAV && sizeof(W) == 4 && NQ == 16 && BP == 64;
     for (int t = tid; t < NP * NP; t += XC_THREADS) {
         const int r = t / NP, c = t % NP;
-        rho[t] = (r < N && c < N) ? (W)rg[r * N + c] : (W)0;
+        const W v = (r < N && c < N) ? (W)rg[r * N + c] : (W)0;
+        if constexpr (MMAT) rho[swz<BP>(r, 16 * (c & 3) + (c >> 2))] = v;
+        else rho[t] = v;
     }
     for (int t = tid; t < 4 * PL; t += XC_THREADS) phi[t] = (W)0;
     for (int sh = tid; sh < nsh; sh += XC_THREADS) {
@@ -354,6 +369,85 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
         xc_eval_phi<W, NQ, BP>(phi, pt, shd, shw, shi, nsh, nb);
         __syncthreads();
         XP(1);
+        if constexpr (MMAT) {
+            // ---- t[p][nu] = sum_mu phi[mu][p] rho[mu][nu] on the tensor cores (3xTF32), then n and
+            // grad n from the accumulator fragments.  M = points: warp w owns the 16 points of m tile
+            // w & 3 and the 32 columns nu = 4 (8 (w >> 2) + n) + j' (n = 0..7 inside n tile j' = 0..3).
+            // K = AOs in a permuted order: step (h, j) covers mu = 4 q + j for the row quads q =
+            // 8 h + 2 k (fragment columns k = 0..3) and 8 h + 2 k + 1 (k = 4..7).  The four rows a
+            // lane group reads in one load then sit in quads whose swizzle keys differ in bits 1-2,
+            // the 8 consecutive columns span two 16-byte groups: 32 different banks (A from the AO
+            // plane, B from the residue-grouped rho, and the AO values of the epilogue alike).
+            const int lane = tid & 31, wp = tid >> 5, g = lane >> 2, tq = lane & 3;
+            const int mt = wp & 3, nh = wp >> 2;
+            const int gA = 4 * mt + (g >> 2), gl = g & 3;        // column group / offset of point 16 mt + g
+            const int gB = 2 * nh + (g >> 2);                    // + 4 j': column group of rho' column 16 j' + 8 nh + g
+            float tacc[4][4];
+#pragma unroll
+            for (int n = 0; n < 4; ++n)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) tacc[n][k] = 0.f;
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                const int q0 = 8 * (ks >> 2) + 2 * tq, q1 = q0 + 1, jr = ks & 3;
+                const float *pa0 = (const float *)phi + (4 * q0 + jr) * BP, *pa1 = (const float *)phi + (4 * q1 + jr) * BP;
+                const float *pb0 = (const float *)rho + (4 * q0 + jr) * NP, *pb1 = (const float *)rho + (4 * q1 + jr) * NP;
+                uint32_t a[4], ah[4], al[4];
+                a[0] = __float_as_uint(pa0[(((gA ^ q0) & 15) << 2) | gl]);
+                a[1] = __float_as_uint(pa0[((((gA + 2) ^ q0) & 15) << 2) | gl]);
+                a[2] = __float_as_uint(pa1[(((gA ^ q1) & 15) << 2) | gl]);
+                a[3] = __float_as_uint(pa1[((((gA + 2) ^ q1) & 15) << 2) | gl]);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) tf32_split(a[k], ah[k], al[k]);
+#pragma unroll
+                for (int n = 0; n < 4; ++n) {
+                    uint32_t b0h, b0l, b1h, b1l;
+                    tf32_split(__float_as_uint(pb0[((((4 * n + gB) ^ q0) & 15) << 2) | gl]), b0h, b0l);
+                    tf32_split(__float_as_uint(pb1[((((4 * n + gB) ^ q1) & 15) << 2) | gl]), b1h, b1l);
+                    mma_tf32(tacc[n], ah, b0l, b1l);
+                    mma_tf32(tacc[n], al, b0h, b1h);
+                    mma_tf32(tacc[n], ah, b0h, b1h);
+                }
+            }
+            // accumulator fragment of n tile j': c0, c1 = (point g, nu(2 tq), nu(2 tq + 1)), c2, c3 = (point g + 8, same)
+            float h8[8];                                        // index 2 * component + point half
+#pragma unroll
+            for (int k = 0; k < 8; ++k) h8[k] = 0.f;
+#pragma unroll
+            for (int n = 0; n < 4; ++n)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int qe = 8 * nh + 2 * tq + e;
+                    const float *pr = (const float *)phi + (4 * qe + n) * BP;
+#pragma unroll
+                    for (int hf = 0; hf < 2; ++hf) {
+                        const float *pp = pr + (((((gA + 2 * hf) ^ qe) & 15) << 2) | gl);
+                        const float tv = tacc[n][2 * hf + e];
+                        h8[hf] = fmaf(tv, pp[0], h8[hf]);
+                        h8[2 + hf] = fmaf(tv, pp[PL], h8[2 + hf]);
+                        h8[4 + hf] = fmaf(tv, pp[2 * PL], h8[4 + hf]);
+                        h8[6 + hf] = fmaf(tv, pp[3 * PL], h8[6 + hf]);
+                    }
+                }
+            // sum over the four lanes of a point pair (transposing butterfly): lane tq ends with
+            // point half tq & 1 and components (tq >> 1) & 1 and 2 + ((tq >> 1) & 1)
+#pragma unroll
+            for (int s_ = 0; s_ < 2; ++s_) {
+                const int o = 1 << s_;
+                const bool up = (tq & o) != 0;
+#pragma unroll
+                for (int k = 0; k < (4 >> s_); ++k) {
+                    const float mine = up ? h8[2 * k + 1] : h8[2 * k], other = up ? h8[2 * k] : h8[2 * k + 1];
+                    h8[k] = mine + __shfl_xor_sync(0xffffffffu, other, o);
+                }
+            }
+            // the two warps that share an m tile (nu halves) leave their sums side by side; the
+            // functional adds them
+            float *part = (float *)dn;                          // [2][BP][4] floats
+            const int pp_ = 16 * mt + g + 8 * (tq & 1), cmp = (tq >> 1) & 1;
+            part[(nh * BP + pp_) * 4 + cmp] = h8[0];
+            part[(nh * BP + pp_) * 4 + 2 + cmp] = h8[1];
+        } else
         {   // ---- t = phi^T rho for 4 points x 4 AOs, then n and grad n partials
             W n4[4] = {0, 0, 0, 0}, g4[3][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}};
 #pragma unroll
@@ -487,10 +581,17 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
         XP(2);
         if (tid < 3 * BP) {   // ---- functional (f64): parts on three thread groups, one point each
             const int pt_i = tid % BP, part = tid / BP;
-            const double *dq = dn + 4 * pt_i;
-            double n = dq[0], sig = 0.0;
+            double n, gxd, gyd, gzd, sig = 0.0;
+            if constexpr (MMAT) {
+                const float4 pa = reinterpret_cast<const float4 *>(dn)[pt_i], pb = reinterpret_cast<const float4 *>(dn)[BP + pt_i];
+                n = (double)(pa.x + pb.x);
+                gxd = (double)(2 * (pa.y + pb.y)); gyd = (double)(2 * (pa.z + pb.z)); gzd = (double)(2 * (pa.w + pb.w));
+            } else {
+                const double *dq = dn + 4 * pt_i;
+                n = dq[0]; gxd = dq[1]; gyd = dq[2]; gzd = dq[3];
+            }
             {
-                const double gx = dq[1], gy = dq[2], gz = dq[3];
+                const double gx = gxd, gy = gyd, gz = gzd;
                 sig = (double)((W)gx * (W)gx + (W)gy * (W)gy + (W)gz * (W)gz);
             }
             const bool ok = pt_i < nb && b3lyp_clamp(n, sig);
@@ -508,9 +609,8 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
             if (part == 0 && ok) x = b3lyp_x(n, sig);
             asm volatile("bar.sync 1, %0;" ::"r"(3 * BP) : "memory");
             if (part == 0) {
-            double *d = dn + 4 * tid;
             if (ok) {
-                const double gx = d[1], gy = d[2], gz = d[3];
+                const double gx = gxd, gy = gyd, gz = gzd;
                 const XCOut o = xc_combine(n, x, VPart{fpt[5 * BP + pt_i], fpt[6 * BP + pt_i]},
                                            LPart{fpt[7 * BP + pt_i], fpt[8 * BP + pt_i], fpt[9 * BP + pt_i]});
                 if (!(isfinite(o.exc) && isfinite(o.vrho) && isfinite(o.vsigma))) bad = 1;
