@@ -380,7 +380,10 @@ int dftb_plan_create(const dftb_batch_in *in, const dftb_opts *opts, void *strea
                 tot += wk[i];
                 wmax = std::max(wmax, wk[i]);
             }
-            const int js = jk_split(nm, opts->precision && !ERI64_F32);
+            int js = jk_split(nm, opts->precision && !ERI64_F32);
+            // f32 store: J_Q is summed in f32 over a CTA's rows - keep that to ~600 rows per CTA on
+            // average for the larger molecules as well (N = 92: 8 CTAs)
+            if (opts->precision && !ERI64_F32) js = std::max(js, (int)((npp + 599) / 600));
             const int64_t target = std::max(wmax, (tot + js - 1) / js);
             int hi = (int)N;
             int64_t acc = 0;
