@@ -237,27 +237,45 @@ def _hbm_peak():
         return 7700.0, "B200_PROFILING.md fallback (HBM3e nominal)"
 
 
+def _source_hash():
+    """md5 over the kernel sources the library is built from (the same function as
+    tools/ncu_summary.py source_hash: csrc/*.cu, *.cuh, Makefile and the C header)."""
+    import glob
+    import hashlib
+
+    c = os.path.join(ROOT, "paper_2311_01135_b200", "csrc")
+    files = sorted(glob.glob(os.path.join(c, "*.cu")) + glob.glob(os.path.join(c, "*.cuh")) +
+                   [os.path.join(c, "Makefile"), os.path.join(ROOT, "include", "qm1b_b200.h")])
+    h = hashlib.md5()
+    for f in files:
+        h.update(os.path.relpath(f, ROOT).encode())
+        h.update(open(f, "rb").read())
+    return h.hexdigest()
+
+
 def _ncu_capture():
     """The newest committed ncu --set full summary (profiles/*_ncu_full_metrics.json, written by
-    tools/prof_r2.sh) whose build hash is the md5 of the library this process runs, else
-    (None, reason): traffic figures are only quoted from a capture of the same build."""
+    tools/prof_r2.sh) of the code this process runs, else (None, reason): traffic figures are only
+    quoted from a capture of the same build.  A capture matches by the md5 of the library it ran
+    or - nvcc output is not bit-reproducible between builds - by the md5 of the kernel sources."""
     import glob
     import hashlib
 
     lib = os.path.join(ROOT, "paper_2311_01135_b200", "libqm1b_b200.so")
     try:
         h = hashlib.md5(open(lib, "rb").read()).hexdigest()
+        hs = _source_hash()
     except OSError:
-        return None, "library missing"
+        return None, "library or sources missing"
     for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_full_metrics.json")), reverse=True):
         try:
             with open(f) as fh:
                 d = json.load(fh)
         except (OSError, ValueError):
             continue
-        if d.get("_build") == h:
+        if d.get("_build") == h or d.get("_src") == hs:
             return d, os.path.relpath(f, ROOT)
-    return None, f"no committed ncu capture of this build (md5 {h[:12]})"
+    return None, f"no committed ncu capture of this build (library md5 {h[:12]}, sources {hs[:12]})"
 
 
 def _dram_bytes(entries):

@@ -38,16 +38,32 @@ def summarize(rep):
 
 
 def build_hash():
-    """md5 of the in-tree library the captures ran (bench.py only uses a summary whose
-    hash matches the library it loads)."""
+    """md5 of the in-tree library the captures ran."""
     import hashlib, os
     lib = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                        "paper_2311_01135_b200", "libqm1b_b200.so")
     return hashlib.md5(open(lib, "rb").read()).hexdigest()
 
 
+def source_hash(root=None):
+    """md5 over the kernel sources the library is built from (csrc/*.cu, *.cuh, Makefile and the C
+    header, names and contents in sorted order).  nvcc's output is not bit-reproducible between
+    builds of the same sources, so bench.py matches a capture to the running code by this hash
+    (the library md5 is kept as well)."""
+    import glob, hashlib, os
+    root = root or os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    c = os.path.join(root, "paper_2311_01135_b200", "csrc")
+    files = sorted(glob.glob(os.path.join(c, "*.cu")) + glob.glob(os.path.join(c, "*.cuh")) +
+                   [os.path.join(c, "Makefile"), os.path.join(root, "include", "qm1b_b200.h")])
+    h = hashlib.md5()
+    for f in files:
+        h.update(os.path.relpath(f, root).encode())
+        h.update(open(f, "rb").read())
+    return h.hexdigest()
+
+
 if __name__ == "__main__":
-    out = {"_build": build_hash()}
+    out = {"_build": build_hash(), "_src": source_hash()}
     for arg in sys.argv[2:]:
         name, rep = arg.split("=", 1)
         out[name] = summarize(rep)
