@@ -124,6 +124,9 @@ __device__ __forceinline__ float ex2_approx(float x) {
 #ifndef XC_MMAV
 #define XC_MMAV 1
 #endif
+#ifndef XC_WV4
+#define XC_WV4 1       // f32 build: wv phase with four points per thread (16-byte loads / stores)
+#endif
 // XC_MMAT=1: the same bucket also runs t = phi^T rho on the tensor cores (see the t phase).
 // Measured on B200 and kept off: kernel 1.60 -> 1.55 ms per iteration, but n = sum_nu t phi
 // inherits the truncating accumulation of a 24-MMA chain and the truncated lo parts as a bias
@@ -630,6 +633,33 @@ __global__ void __launch_bounds__(XC_THREADS, 2) k_xc(DevBatch b, const int *cta
         }
         __syncthreads();
         XP(3);
+        if constexpr (XC_WV4 && sizeof(W) == 4) {
+            // ---- wv = a phi + b . grad phi, four points per thread: the thread's 4-point column group is
+            // fixed (its four coefficient vectors stay in registers), rows in steps of XC_THREADS / (BP / 4);
+            // 16-byte loads and stores (a quarter warp covers 128 contiguous bytes of one row)
+            constexpr int NG = BP / 4, RS = XC_THREADS / NG;
+            const int cg = tid % NG;
+            float c0[4], c1[4], c2[4], c3[4];
+            Vec4<float>::ld((const float *)dw + 4 * cg, c0);
+            Vec4<float>::ld((const float *)dw + BP + 4 * cg, c1);
+            Vec4<float>::ld((const float *)dw + 2 * BP + 4 * cg, c2);
+            Vec4<float>::ld((const float *)dw + 3 * BP + 4 * cg, c3);
+#pragma unroll 2
+            for (int row = tid / NG; row < NP; row += RS) {
+                const int o = row * BP + (((cg ^ (row >> 2)) & (NG - 1)) << 2);
+                float f0[4], f1[4], f2[4], f3[4];
+                Vec4<float>::ld((const float *)phi + o, f0);
+                Vec4<float>::ld((const float *)phi + PL + o, f1);
+                Vec4<float>::ld((const float *)phi + 2 * PL + o, f2);
+                Vec4<float>::ld((const float *)phi + 3 * PL + o, f3);
+                float4 r;
+                r.x = c0[0] * f0[0] + c1[0] * f1[0] + c2[0] * f2[0] + c3[0] * f3[0];
+                r.y = c0[1] * f0[1] + c1[1] * f1[1] + c2[1] * f2[1] + c3[1] * f3[1];
+                r.z = c0[2] * f0[2] + c1[2] * f1[2] + c2[2] * f2[2] + c3[2] * f3[2];
+                r.w = c0[3] * f0[3] + c1[3] * f1[3] + c2[3] * f2[3] + c3[3] * f3[3];
+                *reinterpret_cast<float4 *>((float *)wv + o) = r;
+            }
+        } else
         {   // ---- wv = a phi + b . grad phi; this thread's point is fixed (XC_THREADS % BP == 0)
             static_assert(XC_THREADS % BP == 0, "fixed point per thread");
             const int p = tid % BP;
