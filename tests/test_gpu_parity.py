@@ -429,3 +429,23 @@ def test_f32_jk_every_bucket_vs_f64_accumulation(gpu_lib, sto3g, n_heavy):
     assert np.abs(K32 - K64).max() <= 6e-7 * np.abs(K64).max()
     np.testing.assert_allclose(J32, J32.T, rtol=0, atol=1e-12 * np.abs(J64).max())
     np.testing.assert_allclose(K32, K32.T, rtol=0, atol=1e-12 * np.abs(K64).max())
+
+
+@pytest.mark.parametrize("split", [1, 3, 7, 24])
+def test_f32_jk_under_other_cta_partitions(gpu_lib, split):
+    """The f32 J/K kernel under other CTA partitions of a molecule's slabs than the default (the
+    partition is fixed per process, so each case runs tools/jkerr.py in its own interpreter with
+    QM1B_JK_SPLIT set): different slab ranges, row groups and chunk sizes per CTA.  Errors are
+    against exact f64 sums of the same f32 inputs (dense tensor contraction)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, QM1B_JK_SPLIT=str(split))
+    out = subprocess.run([sys.executable, os.path.join(root, "tools", "jkerr.py")], env=env, cwd=root,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    assert d["J"] < 6e-7 and d["K"] < 6e-7, d
